@@ -1,0 +1,252 @@
+"""Record golden vectors from the REAL reference package -- test infrastructure.
+
+Run in the build container (the only place ``/root/reference`` exists):
+
+    python oracle/make_golden.py
+
+It imports ``fftlasso`` read-only from ``/root/reference/pkg/src``, evaluates
+the hot-path functions on seeded inputs and writes ``tests/golden/*.npz``.
+It also evaluates ``oracle/fftlasso_oracle.py`` on the same inputs and prints
+the worst deviation, so a drifting restatement is caught at generation time;
+``tests/test_oracle_golden.py`` repeats that check on every CPU test run.
+The GPU parity tests compare the CUDA path against these fixtures and the
+oracle.  Nothing here runs on the GPU box.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+OUT = os.path.join(REPO, "tests", "golden")
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import fftlasso as ref  # noqa: E402  (the reference, read-only)
+from fftlasso import ipm as ref_ipm  # noqa: E402
+from fftlasso import newton_system as ref_ns  # noqa: E402
+from fftlasso.pcg import PcgConfig, pcg_solve  # noqa: E402
+
+from oracle import fftlasso_oracle as orc  # noqa: E402
+from paper_2502_04217_b200 import workloads  # noqa: E402
+
+WORST = {}
+
+
+def note(tag, a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    scale = max(1.0, float(np.max(np.abs(a))) if a.size else 1.0)
+    err = float(np.max(np.abs(a - b))) / scale if a.size else 0.0
+    WORST[tag] = max(WORST.get(tag, 0.0), err)
+
+
+def save(name, **arrays):
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"  wrote {os.path.relpath(path, REPO)} ({os.path.getsize(path) // 1024} KiB)")
+
+
+TRANSFORM_DIMS = [(2,), (4,), (6,), (10,), (16,), (64,), (96,), (4096,), (16384,),
+                  (8, 6), (8, 8), (6, 10), (64, 64), (4, 2, 6), (6, 4, 10),
+                  (16, 16, 16), (8, 12, 6), (32, 32, 32)]
+
+
+def transforms():
+    rng = np.random.default_rng(7001)
+    arrays = {}
+    for dims in TRANSFORM_DIMS:
+        g = ref.GridShape(dims)
+        beta = rng.standard_normal(g.n)
+        x = rng.standard_normal(g.n)
+        key = "x".join(map(str, dims))
+        arrays[f"{key}__beta"] = beta
+        arrays[f"{key}__synth"] = ref.synthesize(beta, g)
+        arrays[f"{key}__x"] = x
+        arrays[f"{key}__analyze"] = ref.analyze(x, g)
+        note("synthesize", arrays[f"{key}__synth"], orc.synthesize(beta, dims))
+        note("analyze", arrays[f"{key}__analyze"], orc.analyze(x, dims))
+    arrays["dims_json"] = np.array(json.dumps([list(d) for d in TRANSFORM_DIMS]))
+    save("transforms", **arrays)
+
+
+MASK_CASES = [((64,), 9), ((4096,), 410), ((16, 24), 60), ((8, 12, 16), 200),
+              ((32, 32, 32), 4900)]
+
+
+def masking():
+    rng = np.random.default_rng(7002)
+    arrays = {}
+    for dims, k in MASK_CASES:
+        g = ref.GridShape(dims)
+        miss = np.sort(rng.choice(g.n, k, replace=False))
+        mask = ref.Mask(miss, g)
+        beta = rng.standard_normal(g.n)
+        vals = rng.standard_normal(mask.n_observed)
+        key = "x".join(map(str, dims))
+        arrays[f"{key}__missing"] = miss
+        arrays[f"{key}__beta"] = beta
+        arrays[f"{key}__vals"] = vals
+        arrays[f"{key}__observe"] = ref.observe(beta, mask)
+        arrays[f"{key}__embed"] = ref.embed(vals, mask)
+        arrays[f"{key}__adjoint"] = ref.observe_adjoint(vals, mask)
+        arrays[f"{key}__gram"] = ref.gram(beta, mask)
+        om = orc.make_mask(dims, missing=miss)
+        note("observe", arrays[f"{key}__observe"], orc.observe(beta, om))
+        note("embed", arrays[f"{key}__embed"], orc.embed(vals, om))
+        note("adjoint", arrays[f"{key}__adjoint"], orc.observe_adjoint(vals, om))
+        note("gram", arrays[f"{key}__gram"], orc.gram(beta, om))
+    arrays["cases_json"] = np.array(json.dumps([[list(d), k] for d, k in MASK_CASES]))
+    save("masking", **arrays)
+
+
+def interior_state(rng, n, mu=0.05):
+    """Same distribution as the reference's random_interior_state fixture."""
+    return dict(beta=rng.standard_normal(n) * 0.4, z=rng.random(n) + 0.8,
+                s1=rng.random(n) + 0.4, s2=rng.random(n) + 0.4,
+                y1=rng.random(n) + 0.3, y2=rng.random(n) + 0.3,
+                nu1=rng.random(n) + 0.3, nu2=rng.random(n) + 0.3, mu=mu)
+
+
+NEWTON_CASES = [((64,), 8), ((4, 6, 8), 30), ((32, 32), 150)]
+
+
+def newton():
+    rng = np.random.default_rng(7003)
+    arrays = {}
+    for dims, k in NEWTON_CASES:
+        g = ref.GridShape(dims)
+        n = g.n
+        miss = np.sort(rng.choice(n, k, replace=False))
+        mask = ref.Mask(miss, g)
+        st = interior_state(rng, n)
+        b = rng.standard_normal(mask.n_observed)
+        lam = 0.4
+        rst = ref_ipm.IpmState(**st)
+        d = ref_ns.barrier_diagonals(st["s1"], st["s2"], st["nu1"], st["nu2"])
+        rhs = ref_ns.newton_rhs(rst, b, mask, lam)
+        db = rng.standard_normal(n)
+        dz = rng.standard_normal(n)
+        top, bot = ref_ns.apply_kkt(db, dz, d, mask)
+        ptop, pbot = ref_ns.apply_precond_inverse(db, dz, d)
+        rec = ref_ns.recover_eliminated(db, dz, rhs, d)
+        key = "x".join(map(str, dims))
+        for f in ("beta", "z", "s1", "s2", "y1", "y2", "nu1", "nu2"):
+            arrays[f"{key}__st_{f}"] = st[f]
+        arrays[f"{key}__mu"] = np.array(st["mu"])
+        arrays[f"{key}__lam"] = np.array(lam)
+        arrays[f"{key}__missing"] = miss
+        arrays[f"{key}__b"] = b
+        arrays[f"{key}__db"] = db
+        arrays[f"{key}__dz"] = dz
+        for f in ("sigma1", "sigma2", "lambda1", "lambda2", "dvec", "bvec"):
+            arrays[f"{key}__diag_{f}"] = getattr(d, f)
+        for f in ("r1", "r2", "r3", "r4", "r5", "r6", "r_beta", "r_c"):
+            arrays[f"{key}__rhs_{f}"] = getattr(rhs, f)
+        arrays[f"{key}__kkt_top"] = top
+        arrays[f"{key}__kkt_bottom"] = bot
+        arrays[f"{key}__pinv_top"] = ptop
+        arrays[f"{key}__pinv_bottom"] = pbot
+        for f in ("d_s1", "d_s2", "d_y1", "d_y2"):
+            arrays[f"{key}__rec_{f}"] = getattr(rec, f)
+        # condensed PCG solve at this state (the inner hot loop)
+        res = pcg_solve(lambda v: np.concatenate(ref_ns.apply_kkt(v[:n], v[n:], d, mask)),
+                        lambda v: np.concatenate(ref_ns.apply_precond_inverse(v[:n], v[n:], d)),
+                        np.concatenate([rhs.r_beta, rhs.r_c]),
+                        PcgConfig(abs_tol=1e-12, record_history=True))
+        arrays[f"{key}__pcg_x"] = res.solution
+        arrays[f"{key}__pcg_iters"] = np.array(res.iterations)
+        arrays[f"{key}__pcg_hist"] = np.array(res.residual_history)
+        # oracle cross-check
+        om = orc.make_mask(dims, missing=miss)
+        ost = orc.OState(**{f: st[f].copy() for f in st if f != "mu"}, mu=st["mu"])
+        od = orc.diagonals(st["s1"], st["s2"], st["nu1"], st["nu2"])
+        orhs = orc.newton_rhs(ost, b, om, lam)
+        for i, f in enumerate(("sigma1", "sigma2", "lambda1", "lambda2", "dvec", "bvec")):
+            note("diag(bitwise)", getattr(d, f), od[i])
+        for f in ("r1", "r_beta", "r_c"):
+            note("rhs", getattr(rhs, f), orhs[f])
+        otop, obot = orc.kkt_apply(db, dz, od, om)
+        note("kkt", top, otop)
+        note("kkt", bot, obot)
+        optop, opbot = orc.precond_apply(db, dz, od)
+        note("pinv(bitwise)", ptop, optop)
+        note("pinv(bitwise)", pbot, opbot)
+        ores = orc.pcg(lambda v: np.concatenate(orc.kkt_apply(v[:n], v[n:], od, om)),
+                       lambda v: np.concatenate(orc.precond_apply(v[:n], v[n:], od)),
+                       np.concatenate([orhs["r_beta"], orhs["r_c"]]), history=True)
+        note("pcg", res.solution, ores.solution)
+        assert ores.iterations == res.iterations, (ores.iterations, res.iterations)
+    arrays["cases_json"] = np.array(json.dumps([[list(d), k] for d, k in NEWTON_CASES]))
+    save("newton", **arrays)
+
+
+def _record_solve(name, dims, flags, b, lam, beta_true=None, max_iters=200):
+    g = ref.GridShape(dims)
+    mask = ref.Mask.from_bool(flags, g)
+    cfg = ref_ipm.IpmConfig(lam=lam, tol=1e-8, max_iters=max_iters)
+    beta, rep = ref.solve(b, mask, cfg)
+    om = orc.make_mask(dims, flags=flags)
+    obeta, orep = orc.solve(b, om, orc.OConfig(lam=lam, tol=1e-8, max_iters=max_iters))
+    note("solve beta", beta, obeta)
+    assert orep.krylov_counts == rep.krylov_counts, (name, orep.krylov_counts, rep.krylov_counts)
+    recs = [r.to_dict() for r in rep.records]
+    arrays = dict(dims=np.array(dims), missing=mask.missing, b=b, beta=beta,
+                  lam=np.array(rep.lam), status=np.array(rep.status),
+                  iterations=np.array(rep.iterations),
+                  final_objective=np.array(rep.final_objective),
+                  final_kkt=np.array(rep.final_kkt), final_mu=np.array(rep.final_mu),
+                  records_json=np.array(json.dumps(recs)))
+    if beta_true is not None:
+        arrays["beta_true"] = beta_true
+    save("solve_" + name, **arrays)
+    print(f"    {name}: {rep.status} {rep.iterations} IPM, krylov {rep.krylov_counts}, "
+          f"obj {rep.final_objective:.12e}, lam {rep.lam:.6g}")
+
+
+def _observed(inst):
+    g = ref.GridShape(inst.dims)
+    mask = ref.Mask.from_bool(inst.flags, g)
+    return ref.observe(inst.beta_true, mask) + inst.noise
+
+
+def solves():
+    # C1 at its full size (1D 4096, lambda 0.3) -- SURVEY Appendix A
+    inst = workloads.c1_1d(seed=0)
+    _record_solve("c1_4096", inst.dims, inst.flags, _observed(inst), inst.lam, inst.beta_true)
+    # C2 recipe scaled to 256^2 (same block sizes/density law)
+    inst = workloads.c2_2d(seed=0, n_side=256)
+    _record_solve("c2_256", inst.dims, inst.flags, _observed(inst), inst.lam, inst.beta_true)
+    # C3 recipe at 32^3 and C4/C5 recipe at 32^3
+    inst = workloads.c3_bragg(32, seed=0)
+    _record_solve("c3_32", inst.dims, inst.flags, _observed(inst), inst.lam, inst.beta_true)
+    inst = workloads.c4_const(32)
+    _record_solve("c4_32", inst.dims, inst.flags, _observed(inst), inst.lam, inst.beta_true)
+    # reference's own generator (Appendix B rows 8^3 / 16^3), default lambda
+    for side in (8, 16):
+        noisy, flags, _ = workloads.harmonics((side,) * 3, noise_seed=42, missing_seed=43)
+        _record_solve(f"harm_{side}", (side,) * 3, flags, noisy[~flags], None)
+    # empty mask (pure denoising) and a max_iters best-iterate case
+    rng = np.random.default_rng(7004)
+    b = rng.standard_normal(128)
+    _record_solve("empty_128", (128,), np.zeros(128, bool), b, None)
+    flags = np.zeros(64, bool)
+    flags[rng.choice(64, 9, replace=False)] = True
+    b = rng.standard_normal(64 - 9)
+    _record_solve("maxit_64", (64,), flags, b, 0.4, max_iters=3)
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    print("transforms");  transforms()
+    print("masking");     masking()
+    print("newton");      newton()
+    print("solves");      solves()
+    print("oracle vs reference worst relative deviation:")
+    for k, v in WORST.items():
+        print(f"  {k:16s} {v:.3e}")
