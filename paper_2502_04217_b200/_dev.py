@@ -1,0 +1,113 @@
+"""Device plumbing: torch CUDA buffers, the current stream, plan cache.
+
+PyTorch is used only to own device memory and to name the stream; every
+arithmetic operation on the solver path is a libfftlasso_b200 kernel.
+Functions of the public API accept NumPy arrays (the reference's types --
+results come back as NumPy) or CUDA tensors (results stay on the device).
+"""
+
+from __future__ import annotations
+
+import atexit
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import BackendUnavailableError, UnsupportedShapeError
+
+try:
+    import torch
+except ImportError as exc:  # pragma: no cover - torch is part of the image
+    raise BackendUnavailableError("PyTorch is required for device buffers") from exc
+
+F64 = torch.float64
+
+
+def device() -> "torch.device":
+    if not torch.cuda.is_available():
+        raise BackendUnavailableError("no CUDA device: the B200 path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def is_device(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def to_dev(x, n: int | None = None, what: str = "vector"):
+    """Flat contiguous float64 CUDA tensor view/copy of ``x``."""
+    dev = device()
+    if isinstance(x, torch.Tensor):
+        t = x.detach()
+        if t.device != dev or t.dtype != F64:
+            t = t.to(device=dev, dtype=F64)
+        t = t.reshape(-1)
+        if not t.is_contiguous():
+            t = t.contiguous()
+    else:
+        a = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
+        t = torch.from_numpy(a).to(dev)
+    if n is not None and t.numel() != n:
+        raise UnsupportedShapeError(f"{what} has {t.numel()} entries, expected {n}")
+    return t
+
+
+def empty(n: int):
+    return torch.empty(int(n), dtype=F64, device=device())
+
+
+def zeros(n: int):
+    return torch.zeros(int(n), dtype=F64, device=device())
+
+
+def out(t, like_host: bool):
+    """Return ``t`` as NumPy when the caller passed host data."""
+    return t.cpu().numpy() if like_host else t
+
+
+class Plan:
+    """Owns one fl_plan (per grid shape and device)."""
+
+    def __init__(self, dims, dev_index: int):
+        arr = (ctypes.c_int64 * len(dims))(*dims)
+        h = ctypes.c_void_p()
+        _lib.call("fl_plan_create", len(dims), arr, dev_index, ctypes.byref(h))
+        self.handle = h
+        self.dims = tuple(dims)
+        self.n = int(np.prod(dims))
+
+    def close(self):
+        if self.handle:
+            _lib.lib().fl_plan_destroy(self.handle)
+            self.handle = None
+
+
+_plans: dict = {}
+
+
+def plan_for(dims) -> Plan:
+    dev = device()
+    key = (tuple(int(d) for d in dims), dev.index)
+    p = _plans.get(key)
+    if p is None:
+        p = Plan(key[0], dev.index)
+        _plans[key] = p
+    return p
+
+
+@atexit.register
+def _release_plans():  # pragma: no cover - process teardown
+    for p in _plans.values():
+        try:
+            p.close()
+        except Exception:
+            pass
+    _plans.clear()

@@ -1,0 +1,55 @@
+// Internal (C++) interfaces shared between the translation units of
+// libfftlasso_b200.  Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "fl_fft.cuh"
+
+struct fl_plan {
+  int ndim = 0;
+  int64_t dims[3] = {1, 1, 1};
+  int64_t n = 0;
+  int device = 0;
+  fl::AxisPlan axis[3];
+  std::vector<void*> owned;  // device allocations (twiddle tables)
+};
+
+namespace fl {
+
+enum PassKind : int { K_SYNTH = 0, K_ANALYZE = 1, K_GRAM = 2, K_RESID = 3 };
+
+struct KktEpi {
+  const double* pb = nullptr;   // d_beta
+  const double* pz = nullptr;   // d_z
+  const double* sig1 = nullptr;
+  const double* sig2 = nullptr;
+  double* bottom = nullptr;     // optional
+  double* partials = nullptr;   // non-null: per-block d.Kd partials
+};
+
+// One axis pass over the grid; returns grid size used (for partial slots) in *nblocks.
+int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out,
+             const uint32_t* bits, const double* bhat, const KktEpi* epi, int* nblocks,
+             cudaStream_t s);
+
+// Whole-operator sequences (fl_pass.cu)
+int op_synthesize(const fl_plan* p, const double* in, double* out, cudaStream_t s);
+int op_analyze(const fl_plan* p, const double* in, double* out, cudaStream_t s);
+// gram (resid=false) or A^T Z (bhat - A in) (resid=true); optional KKT epilogue on the last pass.
+int op_gram(const fl_plan* p, const uint32_t* bits, const double* bhat, bool resid,
+            const double* in, double* out, const KktEpi* epi, int* nblocks, cudaStream_t s);
+
+// PCG kernels (fl_vec.cu)
+int pcg_init(int64_t n, const double* sig1, const double* sig2, const double* rhs, double* x,
+             double* r, double* p, double* partials, int* nblocks, cudaStream_t s);
+int pcg_update(int64_t n, const double* sig1, const double* sig2, const double* rho,
+               const double* curv, double* x, double* r, const double* p, const double* kp_top,
+               const double* kp_bot, double* partials, int* nblocks, cudaStream_t s);
+int pcg_pupdate(int64_t n, const double* sig1, const double* sig2, const double* r, double beta,
+                double* p, cudaStream_t s);
+
+}  // namespace fl

@@ -1,0 +1,236 @@
+// Runtime of libfftlasso_b200: error state, per-thread reduction scratch,
+// deterministic reduction finish, plans (radix factorisation + twiddle
+// tables), and the C-ABI entry points of the transform / observation / KKT
+// operators.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fl_common.cuh"
+#include "fl_internal.h"
+
+namespace fl {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+// ---- reduction scratch, one per (host thread, device) ----
+struct ScratchSet {
+  Scratch s[16];
+  ~ScratchSet() {
+    // process teardown: the CUDA context may already be gone, ignore errors
+    for (auto& x : s) {
+      if (x.partials) cudaFree(x.partials);
+      if (x.result) cudaFree(x.result);
+      if (x.host) cudaFreeHost(x.host);
+    }
+  }
+};
+static thread_local ScratchSet g_scratch;
+
+int scratch(Scratch** out) {
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return fail(FL_E_VALUE, "device index out of range");
+  Scratch& s = g_scratch.s[dev];
+  if (!s.partials) {
+    if (cudaMalloc(&s.partials, sizeof(double) * kPartialSlots) != cudaSuccess ||
+        cudaMalloc(&s.result, sizeof(double) * kResultSlots) != cudaSuccess ||
+        cudaMallocHost(&s.host, sizeof(double) * kResultSlots) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FL_E_NOMEM, "cannot allocate reduction scratch");
+    }
+  }
+  *out = &s;
+  return FL_OK;
+}
+
+// One block per reduced row; fixed combine order -> deterministic.
+__global__ void finish_kernel_kinds(const double* __restrict__ partials, int nblocks,
+                                    unsigned long long kindbits, double* __restrict__ result) {
+  __shared__ double red[32];
+  const int row = blockIdx.x;
+  const int kind = (int)((kindbits >> (2 * row)) & 3ull);
+  const double* p = partials + (size_t)row * nblocks;
+  double v = kind == RED_SUM ? 0.0 : (kind == RED_MAX ? -INFINITY : INFINITY);
+  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
+    const double x = p[i];
+    v = kind == RED_SUM ? v + x : (kind == RED_MAX ? fmax(v, x) : fmin(v, x));
+  }
+  if (kind == RED_SUM) v = block_reduce(v, SumOp(), red);
+  else if (kind == RED_MAX) v = block_reduce(v, MaxOp(), red);
+  else v = block_reduce(v, MinOp(), red);
+  if (threadIdx.x == 0) result[row] = v;
+}
+
+int finish_reduce(const double* partials, int nblocks, int nk, const int* kinds, double* result,
+                  cudaStream_t stream) {
+  if (nk > 32) return fail(FL_E_VALUE, "too many reduction rows");
+  unsigned long long bits = 0;
+  for (int k = 0; k < nk; ++k) bits |= (unsigned long long)(kinds[k] & 3) << (2 * k);
+  finish_kernel_kinds<<<nk, 512, 0, stream>>>(partials, nblocks, bits, result);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+int fetch_results(Scratch* s, int count, cudaStream_t stream) {
+  FL_CUDA(cudaMemcpyAsync(s->host, s->result, sizeof(double) * count, cudaMemcpyDeviceToHost, stream));
+  FL_CUDA(cudaStreamSynchronize(stream));
+  return FL_OK;
+}
+
+// ---- plans ----
+static std::vector<int> factor_radices(int m) {
+  std::vector<int> r;
+  while (m % 8 == 0) { r.push_back(8); m /= 8; }
+  while (m % 4 == 0) { r.push_back(4); m /= 4; }
+  while (m % 2 == 0) { r.push_back(2); m /= 2; }
+  for (int p = 3; m > 1; p += 2) {
+    while (m % p == 0) { r.push_back(p); m /= p; }
+    if ((int64_t)p * p > m && m > 1) { r.push_back(m); m = 1; }
+  }
+  return r;
+}
+
+static int build_axis(fl_plan* p, int a) {
+  const int m = (int)p->dims[a];
+  AxisPlan& ap = p->axis[a];
+  ap.m = m;
+  std::vector<int> r = factor_radices(m);
+  if ((int)r.size() > kMaxStages) return fail(FL_E_SHAPE, "too many radix stages");
+  ap.nst = (int)r.size();
+  for (int i = 0; i < ap.nst; ++i) ap.radix[i] = r[i];
+  // twiddles exp(-2 pi i k / m) in extended precision, reduced to the first
+  // octant-free form k/m in [0,1) so the argument carries no error
+  std::vector<double2> tw(m);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int k = 0; k < m; ++k) {
+    const long double ang = two_pi * (long double)k / (long double)m;
+    tw[k].x = (double)cosl(ang);
+    tw[k].y = (double)(-sinl(ang));
+  }
+  // exact values where they are known
+  for (int k = 0; k < m; ++k) {
+    if ((int64_t)4 * k % m == 0) {
+      const int q = (int)((int64_t)4 * k / m);
+      const double c[4] = {1.0, 0.0, -1.0, 0.0}, s[4] = {0.0, -1.0, 0.0, 1.0};
+      tw[k].x = c[q];
+      tw[k].y = s[q];
+    }
+  }
+  void* d = nullptr;
+  FL_CUDA(cudaMalloc(&d, sizeof(double2) * m));
+  p->owned.push_back(d);
+  FL_CUDA(cudaMemcpy(d, tw.data(), sizeof(double2) * m, cudaMemcpyHostToDevice));
+  ap.tw = static_cast<const double2*>(d);
+  return FL_OK;
+}
+
+}  // namespace fl
+
+using namespace fl;
+
+extern "C" {
+
+int fl_version(void) { return 1; }
+
+const char* fl_last_error(void) { return g_err.c_str(); }
+
+int fl_plan_create(int ndim, const int64_t* dims, int device, fl_plan_t* out) {
+  if (!out) return fail(FL_E_VALUE, "null output");
+  *out = nullptr;
+  if (ndim < 1 || ndim > 3) return fail(FL_E_SHAPE, "need 1 to 3 axes, got " + std::to_string(ndim));
+  int64_t n = 1;
+  for (int a = 0; a < ndim; ++a) {
+    if (dims[a] < 2 || dims[a] % 2)
+      return fail(FL_E_SHAPE, "every axis must be even and >= 2, got " + std::to_string(dims[a]));
+    if (dims[a] > (1 << 30)) return fail(FL_E_SHAPE, "axis too long");
+    n *= dims[a];
+  }
+  FL_CUDA(cudaSetDevice(device));
+  fl_plan* p = new fl_plan();
+  p->ndim = ndim;
+  p->n = n;
+  p->device = device;
+  for (int a = 0; a < ndim; ++a) p->dims[a] = dims[a];
+  for (int a = 0; a < ndim; ++a) {
+    int st = build_axis(p, a);
+    if (st != FL_OK) {
+      fl_plan_destroy(p);
+      return st;
+    }
+  }
+  *out = p;
+  return FL_OK;
+}
+
+int fl_plan_destroy(fl_plan_t p) {
+  if (!p) return FL_OK;
+  for (void* d : p->owned) cudaFree(d);
+  delete p;
+  return FL_OK;
+}
+
+int64_t fl_plan_n(fl_plan_t p) { return p ? p->n : -1; }
+
+int fl_synthesize(fl_plan_t p, const double* beta, double* x, fl_stream_t stream) {
+  if (!p || !beta || !x) return fail(FL_E_VALUE, "null argument");
+  return op_synthesize(p, beta, x, (cudaStream_t)stream);
+}
+
+int fl_analyze(fl_plan_t p, const double* x, double* beta, fl_stream_t stream) {
+  if (!p || !beta || !x) return fail(FL_E_VALUE, "null argument");
+  return op_analyze(p, x, beta, (cudaStream_t)stream);
+}
+
+int fl_gram(fl_plan_t p, const uint32_t* bits, const double* beta, double* out, fl_stream_t stream) {
+  if (!p || !bits || !beta || !out) return fail(FL_E_VALUE, "null argument");
+  return op_gram(p, bits, nullptr, false, beta, out, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+int fl_residual_adjoint(fl_plan_t p, const uint32_t* bits, const double* bhat, const double* beta,
+                        double* out, fl_stream_t stream) {
+  if (!p || !bits || !bhat || !out) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!beta) {
+    FL_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * p->n, s));
+    beta = out;
+  }
+  return op_gram(p, bits, bhat, true, beta, out, nullptr, nullptr, s);
+}
+
+int fl_kkt_apply(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2,
+                 const double* d_beta, const double* d_z, double* top, double* bottom,
+                 double* pkp_host, fl_stream_t stream) {
+  if (!p || !bits || !sigma1 || !sigma2 || !d_beta || !d_z || !top)
+    return fail(FL_E_VALUE, "null argument");
+  if (top == d_beta || top == d_z) return fail(FL_E_VALUE, "top must not alias the direction");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc = nullptr;
+  FL_TRY(scratch(&sc));
+  KktEpi e;
+  e.pb = d_beta;
+  e.pz = d_z;
+  e.sig1 = sigma1;
+  e.sig2 = sigma2;
+  e.bottom = bottom;
+  e.partials = pkp_host ? sc->partials : nullptr;
+  int nb = 0;
+  FL_TRY(op_gram(p, bits, nullptr, false, d_beta, top, &e, &nb, s));
+  if (pkp_host) {
+    const int kind = RED_SUM;
+    FL_TRY(finish_reduce(sc->partials, nb, 1, &kind, sc->result, s));
+    FL_TRY(fetch_results(sc, 1, s));
+    *pkp_host = sc->host[0];
+  }
+  return FL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+"""Condensed Newton (KKT) systems, B200 path (reference newton_system.py).
+
+Same public functions and dataclasses as the reference.  The elementwise
+kernels (csrc/fl_vec.cu) evaluate every formula in NumPy's order without
+FMA contraction, so diagonals, right-hand sides, the preconditioner and the
+recovered blocks are bitwise equal to the reference on equal inputs; the
+gram inside ``apply_kkt`` is the fused FFT operator (tolerance-equal).
+
+Block structure (newton_system.py:1-36):
+
+    K = [ G + Lam1   Lam2 ]      P = [ I + Lam1   Lam2 ]
+        [ Lam2       Lam1 ]          [ Lam2       Lam1 ]
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import _dev, _lib
+from .masking import Mask, embed_device
+
+__all__ = [
+    "BarrierDiagonals",
+    "KktRhs",
+    "CondensedSolution",
+    "barrier_diagonals",
+    "newton_rhs",
+    "apply_kkt",
+    "apply_precond_inverse",
+    "apply_precond_kkt",
+    "recover_eliminated",
+]
+
+
+@dataclass(frozen=True)
+class BarrierDiagonals:
+    """Diagonal data of K and P (newton_system.py:60-69); device tensors."""
+
+    sigma1: object
+    sigma2: object
+    lambda1: object
+    lambda2: object
+    dvec: object
+    bvec: object
+
+
+def _vec(x, n=None):
+    return _dev.to_dev(x, n)
+
+
+def barrier_diagonals(s1, s2, nu1, nu2) -> BarrierDiagonals:
+    """sigma = nu/s and the derived diagonals (newton_system.py:72-91).
+
+    Raises InteriorViolationError when any input is <= 0 or non-finite.
+    """
+    host = not _dev.is_device(s1)
+    s1d = _vec(s1)
+    n = s1d.numel()
+    s2d, n1d, n2d = _vec(s2, n), _vec(nu1, n), _vec(nu2, n)
+    outs = [_dev.empty(n) for _ in range(6)]
+    _lib.call("fl_barrier_diagonals", n, *(_dev.ptr(t) for t in (s1d, s2d, n1d, n2d)),
+              *(_dev.ptr(t) for t in outs), _dev.stream())
+    return BarrierDiagonals(*(_dev.out(t, host) for t in outs))
+
+
+@dataclass(frozen=True)
+class KktRhs:
+    """All six block residuals and the condensed pair (newton_system.py:94-110)."""
+
+    r1: object
+    r2: object
+    r3: object
+    r4: object
+    r5: object
+    r6: object
+    r_beta: object
+    r_c: object
+
+
+def fl_state(st) -> _lib.FlState:
+    return _lib.FlState(*(_dev.ptr(getattr(st, f)) for f in
+                          ("beta", "z", "s1", "s2", "y1", "y2", "nu1", "nu2")))
+
+
+def newton_rhs(state, b, mask: Mask, lam: float) -> KktRhs:
+    """Residuals of the barrier KKT system (newton_system.py:113-145)."""
+    from .ipm import as_device_state
+
+    host = not _dev.is_device(state.beta)
+    st = as_device_state(state)
+    n = mask.shape.n
+    diag = barrier_diagonals(st.s1, st.s2, st.nu1, st.nu2)
+    bd = _vec(b, mask.n_observed)
+    bhat = embed_device(bd, mask)
+    plan = _dev.plan_for(mask.shape.dims)
+    g = _dev.empty(n)
+    dm = mask.on_device()
+    _lib.call("fl_residual_adjoint", plan.handle, _dev.ptr(dm.bits), _dev.ptr(bhat),
+              _dev.ptr(st.beta), _dev.ptr(g), _dev.stream())
+    outs = [_dev.empty(n) for _ in range(8)]
+    fs = fl_state(st)
+    _lib.call("fl_newton_rhs", n, _lib.ctypes.byref(fs), _dev.ptr(g), _dev.ptr(diag.sigma1),
+              _dev.ptr(diag.sigma2), float(lam), float(st.mu), *(_dev.ptr(t) for t in outs),
+              _dev.stream())
+    return KktRhs(*(_dev.out(t, host) for t in outs))
+
+
+def apply_kkt(d_beta, d_z, diag: BarrierDiagonals, mask: Mask):
+    """(top, bottom) = K (d_beta, d_z) (newton_system.py:148-152), one fused operator."""
+    host = not _dev.is_device(d_beta)
+    n = mask.shape.n
+    db, dz = _vec(d_beta, n), _vec(d_z, n)
+    top, bot = _dev.empty(n), _dev.empty(n)
+    plan = _dev.plan_for(mask.shape.dims)
+    dm = mask.on_device()
+    g1, g2 = _vec(diag.sigma1, n), _vec(diag.sigma2, n)
+    _lib.call("fl_kkt_apply", plan.handle, _dev.ptr(dm.bits), _dev.ptr(g1), _dev.ptr(g2), _dev.ptr(db), _dev.ptr(dz), _dev.ptr(top), _dev.ptr(bot),
+              None, _dev.stream())
+    return _dev.out(top, host), _dev.out(bot, host)
+
+
+def apply_precond_inverse(r_beta, r_c, diag: BarrierDiagonals):
+    """Closed-form P^{-1} (newton_system.py:155-159)."""
+    host = not _dev.is_device(r_beta)
+    rb = _vec(r_beta)
+    n = rb.numel()
+    rc = _vec(r_c, n)
+    top, bot = _dev.empty(n), _dev.empty(n)
+    g1, g2 = _vec(diag.sigma1, n), _vec(diag.sigma2, n)
+    _lib.call("fl_precond_apply", n, _dev.ptr(g1), _dev.ptr(g2), _dev.ptr(rb),
+              _dev.ptr(rc), _dev.ptr(top), _dev.ptr(bot), _dev.stream())
+    return _dev.out(top, host), _dev.out(bot, host)
+
+
+def apply_precond_kkt(d_beta, d_z, diag: BarrierDiagonals, mask: Mask):
+    """P^{-1} K (newton_system.py:162-165)."""
+    host = not _dev.is_device(d_beta)
+    top, bot = apply_kkt(_vec(d_beta), _vec(d_z), diag, mask)
+    t, b = apply_precond_inverse(top, bot, diag)
+    return _dev.out(t, host), _dev.out(b, host)
+
+
+@dataclass(frozen=True)
+class CondensedSolution:
+    """Full 6-block direction in the symmetrized convention (newton_system.py:168-181)."""
+
+    d_beta: object
+    d_z: object
+    d_s1: object
+    d_s2: object
+    d_y1: object
+    d_y2: object
+
+
+def recover_eliminated(d_beta, d_z, rhs: KktRhs, diag: BarrierDiagonals) -> CondensedSolution:
+    """Back-substitute multipliers and slacks (newton_system.py:184-196)."""
+    host = not _dev.is_device(d_beta)
+    db = _vec(d_beta)
+    n = db.numel()
+    dz = _vec(d_z, n)
+    rs = [_vec(getattr(rhs, f), n) for f in ("r3", "r4", "r5", "r6")]
+    outs = [_dev.empty(n) for _ in range(4)]
+    g1, g2 = _vec(diag.sigma1, n), _vec(diag.sigma2, n)
+    _lib.call("fl_recover_eliminated", n, _dev.ptr(g1), _dev.ptr(g2),
+              *(_dev.ptr(t) for t in rs), _dev.ptr(db), _dev.ptr(dz), *(_dev.ptr(t) for t in outs),
+              _dev.stream())
+    ds1, ds2, dy1, dy2 = (_dev.out(t, host) for t in outs)
+    return CondensedSolution(_dev.out(db, host), _dev.out(dz, host), ds1, ds2, dy1, dy2)

@@ -1,0 +1,161 @@
+"""GPU parity of the operators against the reference's golden vectors.
+
+Mirrors the reference's test_fourier / test_masking / test_newton_system
+strategy: golden vectors recorded from the reference (tests/golden), the
+trig-formula dense matrix, orthogonality, adjointness.  Elementwise KKT
+algebra must be BITWISE equal; transforms within 1e-12 of the reference.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import fftlasso_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+fl = pytest.importorskip("paper_2502_04217_b200")
+from paper_2502_04217_b200 import newton_system as ns  # noqa: E402
+
+
+def _close(a, b, tol):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    scale = max(1.0, float(np.max(np.abs(b))))
+    err = float(np.max(np.abs(a - b))) / scale
+    assert err <= tol, err
+
+
+@pytest.fixture(scope="module")
+def golden_transforms():
+    return load_golden("transforms")
+
+
+def _dims_list(g):
+    return [tuple(d) for d in json.loads(str(g["dims_json"]))]
+
+
+def test_transforms_match_reference(golden_transforms):
+    g = golden_transforms
+    for dims in _dims_list(g):
+        key = "x".join(map(str, dims))
+        shape = fl.GridShape(dims)
+        _close(fl.synthesize(g[key + "__beta"], shape), g[key + "__synth"], 1e-13)
+        _close(fl.analyze(g[key + "__x"], shape), g[key + "__analyze"], 1e-13)
+
+
+@pytest.mark.parametrize("dims", [(2,), (6,), (10,), (16,), (64,), (8, 8), (4, 2, 6), (6, 10, 4),
+                                  (12, 18), (14,), (22,)])
+def test_dense_equivalence(dims):
+    """Columns of A and A^T against the trig formula (test_fourier.py:121-129)."""
+    shape = fl.GridShape(dims)
+    a = orc.dense_synthesis(dims)
+    eye = np.eye(shape.n)
+    a_fast = np.stack([fl.synthesize(e, shape) for e in eye], axis=1)
+    at_fast = np.stack([fl.analyze(e, shape) for e in eye], axis=1)
+    assert np.max(np.abs(a - a_fast)) <= 1e-12
+    assert np.max(np.abs(a.T - at_fast)) <= 1e-12
+
+
+@pytest.mark.parametrize("dims", [(4,), (4096,), (32, 32, 32), (64, 64), (2, 2), (128, 96, 64),
+                                  (2048, 2048), (256, 256, 256)])
+def test_orthogonality_and_isometry(dims, rng):
+    shape = fl.GridShape(dims)
+    beta = rng.standard_normal(shape.n)
+    x = fl.synthesize(beta, shape)
+    assert np.max(np.abs(fl.analyze(x, shape) - beta)) <= 1e-12 * np.max(np.abs(beta))
+    assert abs(np.linalg.norm(x) - np.linalg.norm(beta)) <= 1e-12 * np.linalg.norm(beta)
+
+
+def test_hand_values():
+    """Known answers at m = 4 (test_fourier.py:92-119)."""
+    s2 = np.sqrt(2.0)
+    x = fl.synthesize(np.array([0.5, 0.5, 0.70710678, 0.0]), fl.GridShape((4,)))
+    np.testing.assert_allclose(x, [1.0, 0.0, 0.0, 0.0], atol=1e-8)
+    e2 = np.zeros(4)
+    e2[2] = 1.0
+    np.testing.assert_allclose(fl.synthesize(e2, fl.GridShape((4,))), (s2 / 2) * np.array([1, 0, -1, 0]),
+                               atol=1e-12)
+    xi = fl.analyze(np.array([1.0, 0.0, 0.0, 0.0]), fl.GridShape((4,)))
+    np.testing.assert_allclose(xi, 0.5 * np.array([1, 1, s2, 0]), atol=1e-12)
+    assert np.all(fl.synthesize(np.zeros(16), fl.GridShape((16,))) == 0.0)
+
+
+def test_masking_matches_reference():
+    g = load_golden("masking")
+    for dims, _ in json.loads(str(g["cases_json"])):
+        key = "x".join(map(str, dims))
+        mask = fl.Mask(g[key + "__missing"], fl.GridShape(dims))
+        _close(fl.observe(g[key + "__beta"], mask), g[key + "__observe"], 1e-13)
+        np.testing.assert_array_equal(fl.embed(g[key + "__vals"], mask), g[key + "__embed"])
+        _close(fl.observe_adjoint(g[key + "__vals"], mask), g[key + "__adjoint"], 1e-13)
+        _close(fl.gram(g[key + "__beta"], mask), g[key + "__gram"], 1e-13)
+
+
+def test_gram_properties_large(rng):
+    """Size-independent checks at a C3-sized grid: symmetry, projector, [0,1] spectrum."""
+    from paper_2502_04217_b200 import workloads
+
+    dims = (64, 64, 64)
+    shape = fl.GridShape(dims)
+    mask = fl.Mask.from_bool(workloads.bragg_flags(64), shape)
+    u, v = rng.standard_normal(shape.n), rng.standard_normal(shape.n)
+    gu, gv = fl.gram(u, mask), fl.gram(v, mask)
+    assert abs(u @ gv - v @ gu) <= 1e-11 * abs(u @ gv)
+    # G is an orthogonal projector: G(Gu) = Gu, ||Gu|| <= ||u||
+    np.testing.assert_allclose(fl.gram(gu, mask), gu, atol=1e-12 * np.abs(gu).max())
+    assert np.linalg.norm(gu) <= np.linalg.norm(u)
+    # adjointness of observe / observe_adjoint
+    w = rng.standard_normal(mask.n_observed)
+    assert abs(fl.observe(u, mask) @ w - u @ fl.observe_adjoint(w, mask)) <= 1e-10 * np.linalg.norm(u) * np.linalg.norm(w)
+
+
+def _state(g, key):
+    return orc.OState(**{f: g[f"{key}__st_{f}"].copy() for f in
+                         ("beta", "z", "s1", "s2", "y1", "y2", "nu1", "nu2")},
+                      mu=float(g[key + "__mu"]))
+
+
+def test_newton_system_matches_reference():
+    g = load_golden("newton")
+    from paper_2502_04217_b200.ipm import IpmState
+
+    for dims, _ in json.loads(str(g["cases_json"])):
+        key = "x".join(map(str, dims))
+        mask = fl.Mask(g[key + "__missing"], fl.GridShape(dims))
+        ost = _state(g, key)
+        st = IpmState(mu=ost.mu, **{f: getattr(ost, f) for f in
+                                    ("beta", "z", "s1", "s2", "y1", "y2", "nu1", "nu2")})
+        d = ns.barrier_diagonals(st.s1, st.s2, st.nu1, st.nu2)
+        for f in ("sigma1", "sigma2", "lambda1", "lambda2", "dvec", "bvec"):
+            np.testing.assert_array_equal(getattr(d, f), g[f"{key}__diag_{f}"])
+        rhs = ns.newton_rhs(st, g[key + "__b"], mask, float(g[key + "__lam"]))
+        for f in ("r2", "r3", "r4", "r5", "r6"):
+            np.testing.assert_array_equal(getattr(rhs, f), g[f"{key}__rhs_{f}"])
+        for f in ("r1", "r_beta", "r_c"):
+            _close(getattr(rhs, f), g[f"{key}__rhs_{f}"], 1e-13)
+        top, bot = ns.apply_kkt(g[key + "__db"], g[key + "__dz"], d, mask)
+        _close(top, g[key + "__kkt_top"], 1e-13)
+        np.testing.assert_array_equal(bot, g[key + "__kkt_bottom"])
+        pt, pb = ns.apply_precond_inverse(g[key + "__db"], g[key + "__dz"], d)
+        np.testing.assert_array_equal(pt, g[key + "__pinv_top"])
+        np.testing.assert_array_equal(pb, g[key + "__pinv_bottom"])
+        # recovery from the reference's own rhs -> bitwise
+        ref_rhs = ns.KktRhs(*(g[f"{key}__rhs_{f}"] for f in
+                              ("r1", "r2", "r3", "r4", "r5", "r6", "r_beta", "r_c")))
+        rec = ns.recover_eliminated(g[key + "__db"], g[key + "__dz"], ref_rhs, d)
+        for f in ("d_s1", "d_s2", "d_y1", "d_y2"):
+            np.testing.assert_array_equal(getattr(rec, f), g[f"{key}__rec_{f}"])
+
+
+def test_interior_violation_raises():
+    s = np.ones(8)
+    bad = s.copy()
+    bad[3] = 0.0
+    with pytest.raises(fl.InteriorViolationError):
+        ns.barrier_diagonals(bad, s, s, s)
+    bad[3] = np.nan
+    with pytest.raises(fl.InteriorViolationError):
+        ns.barrier_diagonals(s, s, bad, s)

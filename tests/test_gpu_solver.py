@@ -1,0 +1,187 @@
+"""GPU parity of PCG and the full IPM solve against the reference.
+
+Golden trajectories come from the reference package (tests/golden/solve_*);
+the bar is BASELINE.json's: identical support, objective within 1e-6
+relative, signal within 1e-6 relative l2, IPM iterations within +-1.  We also
+require the per-iteration Krylov counts to match exactly (they do for the
+reference under a different FFT rounding).
+"""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import fftlasso_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+fl = pytest.importorskip("paper_2502_04217_b200")
+from paper_2502_04217_b200 import ipm, newton_system as ns  # noqa: E402
+from paper_2502_04217_b200.pcg import PcgConfig, pcg_solve  # noqa: E402
+
+
+def support(beta):
+    beta = np.asarray(beta)
+    thr = 1e-6 * np.max(np.abs(beta))  # diagnostics.classify_support default
+    return np.flatnonzero(np.abs(beta) > thr)
+
+
+def test_pcg_generic_dense_oracle(rng):
+    """The plug-in interface with NumPy callables (test_pcg.py:72-80)."""
+    q, _ = np.linalg.qr(rng.standard_normal((16, 16)))
+    m = (q * np.geomspace(1.0, 50.0, 16)) @ q.T
+    b = rng.standard_normal(16)
+    res = pcg_solve(lambda v: m @ v, lambda v: v, b, PcgConfig(abs_tol=1e-12))
+    assert res.converged
+    np.testing.assert_allclose(res.solution, np.linalg.solve(m, b), atol=1e-10)
+    ident = pcg_solve(lambda v: v, lambda v: v, b)
+    assert ident.converged and ident.iterations == 1
+    zero = pcg_solve(lambda v: v, lambda v: v, np.zeros(5))
+    assert zero.converged and zero.iterations == 0
+
+
+def test_pcg_breakdown_raises(rng):
+    b = rng.standard_normal(6)
+    with pytest.raises(fl.NumericalBreakdownError):
+        pcg_solve(lambda v: -v, lambda v: v, b)
+    with pytest.raises(fl.NumericalBreakdownError):
+        pcg_solve(lambda v: v * np.nan, lambda v: v, b)
+
+
+def test_kkt_pcg_matches_reference():
+    """Device-resident condensed PCG vs the reference's pcg_solve at fixed states."""
+    g = load_golden("newton")
+    for dims, _ in json.loads(str(g["cases_json"])):
+        key = "x".join(map(str, dims))
+        n = int(np.prod(dims))
+        mask = fl.Mask(g[key + "__missing"], fl.GridShape(dims))
+        st = ipm.IpmState(mu=float(g[key + "__mu"]),
+                          **{f: g[f"{key}__st_{f}"] for f in ipm.FIELDS})
+        d = ns.barrier_diagonals(st.s1, st.s2, st.nu1, st.nu2)
+        rhs = ns.newton_rhs(st, g[key + "__b"], mask, float(g[key + "__lam"]))
+        res = pcg_solve(lambda v: np.concatenate(ns.apply_kkt(v[:n], v[n:], d, mask)),
+                        lambda v: np.concatenate(ns.apply_precond_inverse(v[:n], v[n:], d)),
+                        np.concatenate([rhs.r_beta, rhs.r_c]), PcgConfig(record_history=True))
+        assert res.iterations == int(g[key + "__pcg_iters"])
+        ref = g[key + "__pcg_x"]
+        assert np.linalg.norm(res.solution - ref) <= 1e-9 * np.linalg.norm(ref)
+        # the fused device PCG (what solve() runs)
+        direction = ipm.newton_direction(st, g[key + "__b"], mask, float(g[key + "__lam"]),
+                                         ipm.IpmConfig(lam=float(g[key + "__lam"])))
+        assert direction.krylov_iters == int(g[key + "__pcg_iters"])
+        x = np.concatenate([direction.d_beta, direction.d_z])
+        assert np.linalg.norm(x - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+SOLVES = ["c1_4096", "c2_256", "c3_32", "c4_32", "harm_8", "harm_16", "empty_128", "maxit_64"]
+
+
+@pytest.mark.parametrize("name", SOLVES)
+def test_solve_matches_reference(name):
+    g = load_golden("solve_" + name)
+    dims = tuple(int(d) for d in g["dims"])
+    mask = fl.Mask(g["missing"], fl.GridShape(dims))
+    lam = float(g["lam"])
+    recs = json.loads(str(g["records_json"]))
+    max_iters = 3 if name == "maxit_64" else 200
+    beta, rep = fl.solve(g["b"], mask, fl.IpmConfig(lam=lam, tol=1e-8, max_iters=max_iters))
+    assert rep.status == str(g["status"])
+    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    assert rep.krylov_counts == [r["krylov_iters"] for r in recs]
+    ref = g["beta"]
+    np.testing.assert_array_equal(support(beta), support(ref))
+    obj = float(g["final_objective"])
+    assert abs(rep.final_objective - obj) <= 1e-6 * abs(obj)
+    assert np.linalg.norm(beta - ref) <= 1e-6 * np.linalg.norm(ref)
+    for mine, theirs in zip(rep.records, recs):
+        assert mine.mu == pytest.approx(theirs["mu"], rel=1e-9)
+        assert mine.alpha_primal == pytest.approx(theirs["alpha_primal"], rel=1e-6)
+
+
+def test_default_penalty_recorded(rng):
+    n = 32
+    mask = fl.Mask(np.array([], dtype=np.int64), fl.GridShape((n,)))
+    b = rng.standard_normal(n)
+    beta, rep = fl.solve(b, mask, fl.IpmConfig(tol=1e-8))
+    xi = orc.analyze(b, (n,))
+    assert rep.lam == pytest.approx(0.1 * np.max(np.abs(xi)), rel=1e-14)
+    assert rep.converged and max(rep.krylov_counts) <= 2
+
+
+def test_soft_threshold_closed_form(rng):
+    """Empty mask: the solution is the soft threshold of A^T b (acceptance 2)."""
+    for n in (64, 256):
+        b = rng.standard_normal(n)
+        xi = orc.analyze(b, (n,))
+        lam = 0.3 * np.max(np.abs(xi))
+        mask = fl.Mask(np.array([], dtype=np.int64), fl.GridShape((n,)))
+        beta, rep = fl.solve(b, mask, fl.IpmConfig(lam=lam, tol=1e-8))
+        assert rep.converged
+        st = np.sign(xi) * np.maximum(np.abs(xi) - lam, 0.0)
+        np.testing.assert_allclose(beta, st, atol=1e-7)
+
+
+def test_device_inputs_stay_on_device():
+    import torch
+
+    g = load_golden("solve_c4_32")
+    dims = tuple(int(d) for d in g["dims"])
+    mask = fl.Mask(g["missing"], fl.GridShape(dims))
+    b = torch.from_numpy(g["b"]).cuda()
+    beta, rep = fl.solve(b, mask, fl.IpmConfig(lam=float(g["lam"])))
+    assert isinstance(beta, torch.Tensor) and beta.is_cuda
+    assert rep.converged
+
+
+def test_observer_and_records():
+    g = load_golden("solve_harm_8")
+    mask = fl.Mask(g["missing"], fl.GridShape((8, 8, 8)))
+    seen = []
+    beta, rep = fl.solve(g["b"], mask, fl.IpmConfig(),
+                         observer=lambda s, r: seen.append((s.duality_measure(), r.iteration,
+                                                            float(np.min(s.s1)))))
+    assert [it for _, it, _ in seen] == list(range(1, rep.iterations + 1))
+    assert all(m > 0 for m, _, _ in seen) and all(v > 0 for _, _, v in seen)
+    assert rep.total_krylov == sum(rep.krylov_counts)
+    d = rep.to_dict()
+    assert set(d) == {"record", "status", "iterations", "lambda", "tol", "final_objective",
+                      "final_kkt", "final_mu", "total_krylov", "wall_time"}
+    assert math.isfinite(rep.final_objective)
+
+
+def test_stalled_step_raises(rng, monkeypatch):
+    """Monkeypatched direction that hits the boundary (test_ipm.py:166-182)."""
+    n = 8
+    mask = fl.Mask(np.array([], dtype=np.int64), fl.GridShape((n,)))
+    b = rng.standard_normal(n)
+    state = ipm.initial_state(b, mask, 0.5)
+    z = np.zeros(n)
+    blocked = ipm.NewtonDirection(d_beta=z, d_z=z, d_s1=-1e18 * state.s1, d_s2=z, d_y1=z,
+                                  d_y2=z, d_nu1=z, d_nu2=z, krylov_iters=0, pcg_residual=0.0,
+                                  rhs=None, diag=None)
+    monkeypatch.setattr(ipm, "newton_direction", lambda *a, **k: blocked)
+    with pytest.raises(fl.StalledError):
+        ipm.ipm_step(state, b, mask, 0.5, ipm.IpmConfig(lam=0.5))
+
+
+def test_ipm_step_and_check_convergence_match_oracle(rng):
+    g = load_golden("solve_c1_4096")
+    mask = fl.Mask(g["missing"], fl.GridShape((4096,)))
+    om = orc.make_mask((4096,), missing=g["missing"])
+    lam = float(g["lam"])
+    st = ipm.initial_state(g["b"], mask, lam)
+    ost = orc.initial_state(4096, lam)
+    cfg = ipm.IpmConfig(lam=lam)
+    for _ in range(3):
+        st, d, ap, ad = ipm.ipm_step(st, g["b"], mask, lam, cfg)
+        ost, od, oap, oad = orc.ipm_step(ost, g["b"], om, lam, orc.OConfig(lam=lam))
+        assert d.krylov_iters == od["krylov_iters"]
+        assert ap == pytest.approx(oap, rel=1e-9) and ad == pytest.approx(oad, rel=1e-9)
+    c = ipm.check_convergence(st, g["b"], mask, lam, tol=1e-8)
+    oc = orc.kkt_check(ost, g["b"], om, lam, 1e-8)
+    for f in ("stationarity", "dual_equality", "multiplier_gap", "primal", "complementarity"):
+        assert getattr(c, f) == pytest.approx(oc[f], rel=1e-7)
+    assert c.centrality_ok == oc["centrality_ok"]
