@@ -137,6 +137,13 @@ FL_API int fl_barrier_diagonals(int64_t n, const double* s1, const double* s2, c
 FL_API int fl_kkt_apply(fl_plan_t plan, const uint32_t* miss_bits, const double* sigma1,
                  const double* sigma2, const double* d_beta, const double* d_z, double* top,
                  double* bottom, double* pkp_host, fl_stream_t stream);
+/* fl_kkt_apply with a cudaEvent after every HBM pass; writes the per-pass
+ * device times (ms) to ``pass_ms`` (host, 2*ndim-1 entries) and returns the
+ * number of passes in ``npasses``.  Measurement hook for bench.py. */
+FL_API int fl_kkt_apply_profiled(fl_plan_t plan, const uint32_t* miss_bits, const double* sigma1,
+                                 const double* sigma2, const double* d_beta, const double* d_z,
+                                 double* top, double* bottom, double* pass_ms, int* npasses,
+                                 fl_stream_t stream);
 /* apply_precond_inverse (newton_system.py:155-159). */
 FL_API int fl_precond_apply(int64_t n, const double* sigma1, const double* sigma2, const double* r_beta,
                      const double* r_c, double* top, double* bottom, fl_stream_t stream);

@@ -45,9 +45,18 @@ __device__ __forceinline__ double warp_reduce(double v, Op op) {
   return v;
 }
 
-struct SumOp { __device__ double operator()(double a, double b) const { return a + b; } };
-struct MaxOp { __device__ double operator()(double a, double b) const { return fmax(a, b); } };
-struct MinOp { __device__ double operator()(double a, double b) const { return fmin(a, b); } };
+struct SumOp {
+  static constexpr double identity = 0.0;
+  __device__ double operator()(double a, double b) const { return a + b; }
+};
+struct MaxOp {
+  static constexpr double identity = -__builtin_huge_val();
+  __device__ double operator()(double a, double b) const { return fmax(a, b); }
+};
+struct MinOp {
+  static constexpr double identity = __builtin_huge_val();
+  __device__ double operator()(double a, double b) const { return fmin(a, b); }
+};
 
 // Reduce one value per thread to thread 0 of the block.  ``red`` must hold
 // 32 doubles.  Deterministic: the combine order depends only on blockDim.
@@ -60,7 +69,7 @@ __device__ __forceinline__ double block_reduce(double v, Op op, double* red) {
   __syncthreads();
   const int nw = (blockDim.x + 31) >> 5;
   if (warp == 0) {
-    v = lane < nw ? red[lane] : red[0];
+    v = lane < nw ? red[lane] : Op::identity;
     v = warp_reduce(v, op);
   }
   return v;  // valid in thread 0

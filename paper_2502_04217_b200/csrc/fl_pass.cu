@@ -283,7 +283,10 @@ KernelFn pick_kernel(int kind, bool epi) {
 
 int set_smem_attr(KernelFn k) {
   static_assert(kSmemBudget <= 227 * 1024, "smem budget");
-  FL_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  cudaFuncAttributes fa;
+  FL_CUDA(cudaFuncGetAttributes(&fa, k));
+  const int limit = 227 * 1024 - (int)fa.sharedSizeBytes;
+  FL_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
   return FL_OK;
 }
 
@@ -315,7 +318,7 @@ int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out
   }
   A.fs = A.m + 1;
   const int per_fibre = 2 * A.fs * (int)sizeof(double2);
-  if (per_fibre > 227 * 1024)
+  if (per_fibre > 226 * 1024)
     return fail(FL_E_SHAPE, "axis length " + std::to_string(A.m) + " exceeds the shared-memory FFT limit");
   int F = std::max(1, std::min(16, kSmemBudget / per_fibre));
   if (F >= 8) F = F / 8 * 8;

@@ -25,8 +25,14 @@ __device__ __forceinline__ double nanmax(double a, double b) {
 __device__ __forceinline__ double nanmin(double a, double b) {
   return (isnan(a) || isnan(b)) ? NAN : fmin(a, b);
 }
-struct NanMaxOp { __device__ double operator()(double a, double b) const { return nanmax(a, b); } };
-struct NanMinOp { __device__ double operator()(double a, double b) const { return nanmin(a, b); } };
+struct NanMaxOp {
+  static constexpr double identity = -__builtin_huge_val();
+  __device__ double operator()(double a, double b) const { return nanmax(a, b); }
+};
+struct NanMinOp {
+  static constexpr double identity = __builtin_huge_val();
+  __device__ double operator()(double a, double b) const { return nanmin(a, b); }
+};
 
 template <class Op>
 __device__ __forceinline__ void emit(double v, Op op, double* red, double* partials, int row) {
