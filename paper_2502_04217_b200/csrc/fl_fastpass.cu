@@ -1,0 +1,257 @@
+// Register-resident axis passes for power-of-two fibre lengths 16..8192
+// (the hot path at every BASELINE size).  Same data model and fusion as the
+// generic passes in fl_pass.cu (paired fibres, pack/unpack + ortho scale in
+// the load/store stages, one fused last-axis synth+mask+analysis pass, KKT
+// epilogue in the final store), with the FFT held in registers:
+//
+//   synthesis   global rows (j+1, j+h) -> unpack -> smem -> registers ->
+//               inverse FFT (NST-1 smem exchanges) -> registers -> global
+//   analysis    global -> registers -> forward FFT -> smem -> pack -> global
+//   gram/resid  unpack -> inverse FFT -> mask (in registers) -> forward FFT
+//               (consumes the inverse FFT's register layout directly) -> pack
+//
+// A persistent grid (resident CTAs x 148 SMs) walks the tiles.
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "fl_common.cuh"
+#include "fl_fast.cuh"
+#include "fl_internal.h"
+#include "fl_passargs.cuh"
+
+namespace fl {
+namespace {
+
+using fast::Geom;
+using fast::si;
+
+template <bool STRIDED>
+__device__ __forceinline__ void lane_map(int tid, int W, int P, int& c, int& q) {
+  if (STRIDED) { c = tid % W; q = tid / W; }  // fibre-fast: 128-byte row segments per quarter-warp
+  else { q = tid % P; c = tid / P; }          // position-fast: contiguous rows
+}
+
+template <int M, bool STRIDED, int KIND, bool EPI>
+__global__ void __launch_bounds__(Geom<M>::T, (KIND == K_GRAM || KIND == K_RESID) ? 1 : Geom<M>::MINB) fast_pass(const PassArgs A) {
+  using G = Geom<M>;
+  constexpr int E = G::E, P = G::P, W = G::W, H = M / 2;
+  extern __shared__ double2 smem[];
+  __shared__ double red[32];
+  int c, q;
+  lane_map<STRIDED>(threadIdx.x, W, P, c, q);
+  double2* fib = smem + c * G::FS;
+  const double2* tw = A.plan.tw;
+  const double c0 = A.c0, c1 = A.c1;
+  double acc = 0.0;
+  const int64_t ntiles = (A.G + W - 1) / W;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t g = tile * W + c;
+    const bool valid = g < A.G;
+    const Geo Q = geo<STRIDED>(A, valid ? g : 0);
+    double2 v[E];
+    if (KIND == K_ANALYZE) {
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const int t = q + r * P;
+        double2 z = make_double2(0.0, 0.0);
+        if (valid) {
+          if (STRIDED) z = *reinterpret_cast<const double2*>(A.in + Q.bx + t * Q.st);
+          else {
+            z.x = A.in[Q.bx + t];
+            if (Q.by >= 0) z.y = A.in[Q.by + t];
+          }
+        }
+        v[r] = z;
+      }
+      fast::fft<M>(v, fib, q, tw, -1);
+    } else {
+      // unpack packed rows (j+1, j+h) into the combined half spectra Zin_j, Zin_{M-j}
+#pragma unroll
+      for (int r = 0; r < E / 2; ++r) {
+        const int j = q + r * P;
+        const int64_t ia = Q.st * (j ? j + 1 : 0), ib = Q.st * (j ? j + H : 1);
+        double xa = 0.0, xb = 0.0, ya = 0.0, yb = 0.0;
+        if (valid) {
+          if (STRIDED) {
+            const double2 a = *reinterpret_cast<const double2*>(A.in + Q.bx + ia);
+            const double2 b = *reinterpret_cast<const double2*>(A.in + Q.bx + ib);
+            xa = a.x; ya = a.y; xb = b.x; yb = b.y;
+          } else {
+            xa = A.in[Q.bx + ia];
+            xb = A.in[Q.bx + ib];
+            if (Q.by >= 0) { ya = A.in[Q.by + ia]; yb = A.in[Q.by + ib]; }
+          }
+        }
+        if (j == 0) {
+          fib[si(0)] = make_double2(c0 * xa, c0 * ya);
+          fib[si(H)] = make_double2(c0 * xb, c0 * yb);
+        } else {
+          fib[si(j)] = make_double2(c1 * (xa - yb), c1 * (xb + ya));
+          fib[si(M - j)] = make_double2(c1 * (xa + yb), c1 * (ya - xb));
+        }
+      }
+      __syncthreads();
+      fast::load_natural<M>(v, fib, q);
+      __syncthreads();
+      fast::fft<M>(v, fib, q, tw, +1);
+      if (KIND == K_SYNTH) {
+        if (valid) {
+#pragma unroll
+          for (int r = 0; r < E; ++r) {
+            const int t = q + r * P;
+            if (STRIDED) *reinterpret_cast<double2*>(A.out + Q.bx + t * Q.st) = v[r];
+            else {
+              A.out[Q.bx + t] = v[r].x;
+              if (Q.by >= 0) A.out[Q.by + t] = v[r].y;
+            }
+          }
+        }
+      } else {
+        // Z (b_hat - x) or Z x on the synthesized samples, in registers
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int t = q + r * P;
+          double2 z = v[r];
+          if (valid) {
+            const int64_t vx = Q.bx + t;
+            if (KIND == K_RESID) z.x = missing(A.bits, vx) ? 0.0 : A.bhat[vx] - z.x;
+            else if (missing(A.bits, vx)) z.x = 0.0;
+            if (Q.by >= 0) {
+              const int64_t vy = Q.by + t;
+              if (KIND == K_RESID) z.y = missing(A.bits, vy) ? 0.0 : A.bhat[vy] - z.y;
+              else if (missing(A.bits, vy)) z.y = 0.0;
+            } else {
+              z.y = 0.0;
+            }
+          }
+          v[r] = z;
+        }
+        fast::fft<M>(v, fib, q, tw, -1);
+      }
+    }
+    if (KIND != K_SYNTH) {
+      fast::store_natural<M>(v, fib, q);
+      __syncthreads();
+      if (valid) {
+#pragma unroll
+        for (int r = 0; r < E / 2; ++r) {
+          const int j = q + r * P;
+          double xa, xb, ya, yb;
+          if (j == 0) {
+            const double2 z0 = fib[si(0)], zh = fib[si(H)];
+            xa = c0 * z0.x; ya = c0 * z0.y;
+            xb = c0 * zh.x; yb = c0 * zh.y;
+          } else {
+            const double2 a = fib[si(j)], b = fib[si(M - j)];
+            xa = c1 * (a.x + b.x);
+            xb = c1 * (a.y - b.y);
+            ya = c1 * (a.y + b.y);
+            yb = c1 * (b.x - a.x);
+          }
+          const int64_t ia = Q.st * (j ? j + 1 : 0), ib = Q.st * (j ? j + H : 1);
+          if (STRIDED && !EPI) {
+            *reinterpret_cast<double2*>(A.out + Q.bx + ia) = make_double2(xa, ya);
+            *reinterpret_cast<double2*>(A.out + Q.bx + ib) = make_double2(xb, yb);
+          } else {
+            put<STRIDED, EPI>(A, Q.bx + ia, xa, acc);
+            put<STRIDED, EPI>(A, Q.bx + ib, xb, acc);
+            if (Q.by >= 0) {
+              put<STRIDED, EPI>(A, Q.by + ia, ya, acc);
+              put<STRIDED, EPI>(A, Q.by + ib, yb, acc);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (EPI && A.epi.partials) {
+    const double s = block_reduce(acc, SumOp(), red);
+    if (threadIdx.x == 0) A.epi.partials[blockIdx.x] = s;
+  }
+}
+
+struct Entry {
+  KernelFn fn = nullptr;
+  int threads = 0, smem = 0, grid = 0;
+};
+
+template <int M, bool S>
+Entry make(int kind, bool epi) {
+  Entry e;
+  using G = Geom<M>;
+  switch (kind) {
+    case K_SYNTH: e.fn = fast_pass<M, S, K_SYNTH, false>; break;
+    case K_ANALYZE: e.fn = epi ? fast_pass<M, S, K_ANALYZE, true> : fast_pass<M, S, K_ANALYZE, false>; break;
+    case K_GRAM:
+      if constexpr (!S) e.fn = epi ? fast_pass<M, false, K_GRAM, true> : fast_pass<M, false, K_GRAM, false>;
+      break;
+    default:
+      if constexpr (!S) e.fn = epi ? fast_pass<M, false, K_RESID, true> : fast_pass<M, false, K_RESID, false>;
+      break;
+  }
+  e.threads = G::T;
+  e.smem = G::SMEM;
+  return e;
+}
+
+template <bool S>
+Entry lookup(int m, int kind, bool epi) {
+  switch (m) {
+    case 16: return make<16, S>(kind, epi);
+    case 32: return make<32, S>(kind, epi);
+    case 64: return make<64, S>(kind, epi);
+    case 128: return make<128, S>(kind, epi);
+    case 256: return make<256, S>(kind, epi);
+    case 512: return make<512, S>(kind, epi);
+    case 1024: return make<1024, S>(kind, epi);
+    case 2048: return make<2048, S>(kind, epi);
+    case 4096: return make<4096, S>(kind, epi);
+    case 8192: return make<8192, S>(kind, epi);
+    default: return Entry();
+  }
+}
+
+int grid_of(Entry& e, int* out) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    FL_CUDA(cudaGetDevice(&dev));
+    FL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  cudaFuncAttributes fa;
+  FL_CUDA(cudaFuncGetAttributes(&fa, e.fn));
+  FL_CUDA(cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               227 * 1024 - (int)fa.sharedSizeBytes));
+  int per_sm = 0;
+  FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e.fn, e.threads, e.smem));
+  if (per_sm < 1) return fail(FL_E_CUDA, "fast pass kernel cannot be resident");
+  *out = per_sm * sms;
+  return FL_OK;
+}
+
+}  // namespace
+
+bool fast_supported(int m) { return m >= 16 && m <= 8192 && (m & (m - 1)) == 0; }
+
+int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int* nblocks,
+                cudaStream_t s) {
+  // per (m, layout, kind, epi) cache of the persistent grid size
+  static int cache[14][2][4][2] = {};
+  int lg = 0;
+  while ((1 << lg) < m) ++lg;
+  Entry e = strided ? lookup<true>(m, kind, epi) : lookup<false>(m, kind, epi);
+  if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");
+  int& grid_cap = cache[lg][strided][kind][epi];
+  if (!grid_cap) FL_TRY(grid_of(e, &grid_cap));
+  const int W = e.threads / (m / (m >= 1024 ? 16 : 8));
+  const int64_t tiles = (A.G + W - 1) / W;
+  const int grid = (int)std::min<int64_t>(tiles, grid_cap);
+  e.fn<<<grid, e.threads, e.smem, s>>>(A);
+  FL_LAUNCH_CHECK();
+  if (nblocks) *nblocks = grid;
+  return FL_OK;
+}
+
+}  // namespace fl

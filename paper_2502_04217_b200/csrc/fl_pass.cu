@@ -20,10 +20,12 @@
 // fibres), so no scratch vector is needed.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "fl_common.cuh"
 #include "fl_internal.h"
+#include "fl_passargs.cuh"
 
 namespace fl {
 
@@ -32,65 +34,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kMaxGrid = 148 * 16;
-
-struct PassArgs {
-  const double* in;
-  double* out;
-  int64_t G;      // fibre pairs
-  int64_t inner;  // strided: element stride (doubles); also pairs-per-outer * 2
-  int m, h;
-  int has_y;
-  int F, fs;
-  double c0, c1;  // 1/sqrt(m), 1/sqrt(2m)
-  AxisPlan plan;
-  const uint32_t* bits;
-  const double* bhat;
-  KktEpi epi;
-};
-
-// Geometry of fibre pair g: element k of fibre x at bx + k*st, of y at by + k*st.
-struct Geo {
-  int64_t bx, by, st;
-};
-
-template <bool STRIDED>
-__device__ __forceinline__ Geo geo(const PassArgs& A, int64_t g) {
-  Geo r;
-  if (STRIDED) {
-    const int64_t ppo = A.inner >> 1;
-    const int64_t o = g / ppo, q = g - o * ppo;
-    r.bx = o * (int64_t)A.m * A.inner + 2 * q;
-    r.by = r.bx + 1;
-    r.st = A.inner;
-  } else {
-    r.bx = A.has_y ? 2 * g * (int64_t)A.m : g * (int64_t)A.m;
-    r.by = A.has_y ? r.bx + A.m : -1;
-    r.st = 1;
-  }
-  return r;
-}
-
-__device__ __forceinline__ bool missing(const uint32_t* bits, int64_t v) {
-  return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
-}
-
-// KKT epilogue at voxel v with gram value gv (NumPy order, no FMA).
-__device__ __forceinline__ void kkt_store(const PassArgs& A, int64_t v, double gv, double& acc) {
-  const double pb = A.epi.pb[v], pz = A.epi.pz[v];
-  const double s1 = A.epi.sig1[v], s2 = A.epi.sig2[v];
-  const double l1 = add(s1, s2), l2 = sub(s1, s2);
-  const double top = add(add(gv, mul(l1, pb)), mul(l2, pz));
-  const double bot = add(mul(l2, pb), mul(l1, pz));
-  A.out[v] = top;
-  if (A.epi.bottom) A.epi.bottom[v] = bot;
-  acc += pb * top + pz * bot;
-}
-
-template <bool STRIDED, bool EPI>
-__device__ __forceinline__ void put(const PassArgs& A, int64_t v, double val, double& acc) {
-  if (EPI) kkt_store(A, v, val, acc);
-  else A.out[v] = val;
-}
 
 // Mapping of a linear work index onto (fibre f, position j) so that the
 // global side is coalesced: fibre-fast on strided axes, position-fast on
@@ -269,8 +212,6 @@ __global__ void __launch_bounds__(kThreads) axis_pass(const PassArgs A) {
   }
 }
 
-using KernelFn = void (*)(const PassArgs);
-
 template <bool S>
 KernelFn pick_kernel(int kind, bool epi) {
   switch (kind) {
@@ -316,6 +257,18 @@ int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out
     A.has_y = outer >= 2;
     A.G = A.has_y ? outer / 2 : 1;
   }
+  A.c0 = 1.0 / std::sqrt((double)A.m);
+  A.c1 = 1.0 / std::sqrt(2.0 * (double)A.m);
+  A.plan = p->axis[axis];
+  A.bits = bits;
+  A.bhat = bhat;
+  if (epi) A.epi = *epi;
+  static const bool force_generic = [] {
+    const char* e = std::getenv("FL_FORCE_GENERIC");
+    return e && e[0] == '1';
+  }();
+  if (!force_generic && fast_supported(A.m))
+    return launch_fast(A.m, strided, kind, epi != nullptr, A, nblocks, s);
   A.fs = A.m + 1;
   const int per_fibre = 2 * A.fs * (int)sizeof(double2);
   if (per_fibre > 226 * 1024)
@@ -324,12 +277,6 @@ int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out
   if (F >= 8) F = F / 8 * 8;
   if ((int64_t)F > A.G) F = (int)A.G;
   A.F = F;
-  A.c0 = 1.0 / std::sqrt((double)A.m);
-  A.c1 = 1.0 / std::sqrt(2.0 * (double)A.m);
-  A.plan = p->axis[axis];
-  A.bits = bits;
-  A.bhat = bhat;
-  if (epi) A.epi = *epi;
   const bool has_epi = epi != nullptr;
   KernelFn k = strided ? pick_kernel<true>(kind, has_epi) : pick_kernel<false>(kind, has_epi);
   bool& done = attrs_set[strided][kind][has_epi];
