@@ -9,12 +9,21 @@
 
 #include "fl_fft.cuh"
 
+// Four-step decomposition of an axis too long for one CTA's shared memory.
+struct LongAxis {
+  bool on = false;
+  int m1 = 0, m2 = 0;
+  fl::AxisPlan p1, p2;
+  double2* scratch = nullptr;  // G * m complex
+};
+
 struct fl_plan {
   int ndim = 0;
   int64_t dims[3] = {1, 1, 1};
   int64_t n = 0;
   int device = 0;
   fl::AxisPlan axis[3];
+  LongAxis lng[3];
   std::vector<void*> owned;  // device allocations (twiddle tables)
 };
 
@@ -35,6 +44,11 @@ struct KktEpi {
 int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out,
              const uint32_t* bits, const double* bhat, const KktEpi* epi, int* nblocks,
              cudaStream_t s);
+
+struct PassArgs;
+int long_factor(int m, int* m1, int* m2);
+int run_long(const fl_plan* p, int axis, int kind, const PassArgs& A, bool strided, const KktEpi* epi,
+             int* nblocks, cudaStream_t s);
 
 // Whole-operator sequences (fl_pass.cu)
 int op_synthesize(const fl_plan* p, const double* in, double* out, cudaStream_t s);

@@ -263,6 +263,7 @@ int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out
   A.bits = bits;
   A.bhat = bhat;
   if (epi) A.epi = *epi;
+  if (p->lng[axis].on) return run_long(p, axis, kind, A, strided, epi, nblocks, s);
   static const bool force_generic = [] {
     const char* e = std::getenv("FL_FORCE_GENERIC");
     return e && e[0] == '1';

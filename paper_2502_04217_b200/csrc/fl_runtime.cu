@@ -99,25 +99,19 @@ static std::vector<int> factor_radices(int m) {
   return r;
 }
 
-static int build_axis(fl_plan* p, int a) {
-  const int m = (int)p->dims[a];
-  AxisPlan& ap = p->axis[a];
+static int make_axis_plan(fl_plan* p, int m, AxisPlan& ap) {
   ap.m = m;
   std::vector<int> r = factor_radices(m);
   if ((int)r.size() > kMaxStages) return fail(FL_E_SHAPE, "too many radix stages");
   ap.nst = (int)r.size();
   for (int i = 0; i < ap.nst; ++i) ap.radix[i] = r[i];
-  // twiddles exp(-2 pi i k / m) in extended precision, reduced to the first
-  // octant-free form k/m in [0,1) so the argument carries no error
+  // twiddles exp(-2 pi i k / m) in extended precision; exact at the quarter turns
   std::vector<double2> tw(m);
   const long double two_pi = 6.283185307179586476925286766559005768L;
   for (int k = 0; k < m; ++k) {
     const long double ang = two_pi * (long double)k / (long double)m;
     tw[k].x = (double)cosl(ang);
     tw[k].y = (double)(-sinl(ang));
-  }
-  // exact values where they are known
-  for (int k = 0; k < m; ++k) {
     if ((int64_t)4 * k % m == 0) {
       const int q = (int)((int64_t)4 * k / m);
       const double c[4] = {1.0, 0.0, -1.0, 0.0}, s[4] = {0.0, -1.0, 0.0, 1.0};
@@ -130,6 +124,32 @@ static int build_axis(fl_plan* p, int a) {
   p->owned.push_back(d);
   FL_CUDA(cudaMemcpy(d, tw.data(), sizeof(double2) * m, cudaMemcpyHostToDevice));
   ap.tw = static_cast<const double2*>(d);
+  return FL_OK;
+}
+
+// Largest axis the single-CTA shared-memory engines handle: power-of-two
+// lengths up to 8192 (register engine), others while two fibre buffers fit.
+static bool fits_one_cta(int m) {
+  if (m <= 8192 && (m & (m - 1)) == 0) return true;
+  return 2 * (m + 1) * 16 <= 226 * 1024;
+}
+
+static int build_axis(fl_plan* p, int a) {
+  const int m = (int)p->dims[a];
+  FL_TRY(make_axis_plan(p, m, p->axis[a]));
+  if (fits_one_cta(m)) return FL_OK;
+  LongAxis& la = p->lng[a];
+  FL_TRY(long_factor(m, &la.m1, &la.m2));
+  FL_TRY(make_axis_plan(p, la.m1, la.p1));
+  FL_TRY(make_axis_plan(p, la.m2, la.p2));
+  // fibre pairs of this axis times m complex entries
+  int64_t pairs = p->n / m / 2;
+  if (pairs < 1) pairs = 1;
+  void* d = nullptr;
+  FL_CUDA(cudaMalloc(&d, sizeof(double2) * (size_t)pairs * m));
+  p->owned.push_back(d);
+  la.scratch = static_cast<double2*>(d);
+  la.on = true;
   return FL_OK;
 }
 
