@@ -31,17 +31,34 @@ template <int M>
 struct Geom {
   static constexpr int E = M >= 1024 ? 16 : 8;                  // elements per thread
   static constexpr int P = M / E;                               // threads per fibre
-  static constexpr int T = M <= 512 ? 512 : imax(256, P);       // threads per CTA
+  static constexpr int T = imax(256, P);                        // threads per CTA
   static constexpr int W = T / P;                               // fibres per CTA tile
   static constexpr int FS = M + M / 8 + 1;                      // smem fibre stride (double2)
-  static constexpr int SMEM = W * FS * 16;                      // bytes
-  static constexpr int MINB = M <= 512 ? 2 : 1;                 // resident CTAs targeted per SM
+  static constexpr int FIB_BYTES = W * FS * 16;                 // exchange buffer
+  static constexpr int STAGE_BYTES = W * M * 16;                // one raw input tile
+  // cp.async double buffering of the next tile while the current one computes
+  static constexpr bool PIPE = FIB_BYTES + 2 * STAGE_BYTES <= 113 * 1024;
+  static constexpr int SMEM = FIB_BYTES + (PIPE ? 2 * STAGE_BYTES : 0);
+  static constexpr int MINB = PIPE ? 2 : 1;                     // resident CTAs targeted per SM
   static constexpr int NFULL = nfull(M, E);
   static constexpr int REM = M / ipow(E, NFULL);                // first-stage radix if > 1
   static constexpr int NST = NFULL + (REM > 1 ? 1 : 0);
   static constexpr int radix(int s) { return (REM > 1 && s == 0) ? REM : E; }
   static constexpr int ns(int s) { return s == 0 ? 1 : ns(s - 1) * radix(s - 1); }
 };
+
+// ---- cp.async (LDGSTS) helpers ----
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // ---- DFT kernels on register arrays (stride-aware) ----
 template <int R, int STRIDE>

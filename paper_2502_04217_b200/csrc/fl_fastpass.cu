@@ -25,6 +25,10 @@ namespace {
 
 using fast::Geom;
 using fast::si;
+using fast::cp_async16;
+using fast::cp_async8;
+using fast::cp_commit;
+using fast::cp_wait;
 
 template <bool STRIDED>
 __device__ __forceinline__ void lane_map(int tid, int W, int P, int& c, int& q) {
@@ -32,57 +36,120 @@ __device__ __forceinline__ void lane_map(int tid, int W, int P, int& c, int& q) 
   else { q = tid % P; c = tid / P; }          // position-fast: contiguous rows
 }
 
+// 16-byte KKT epilogue for a strided-axis pair (x at v, y at v + 1).
+__device__ __forceinline__ void kkt_store2(const PassArgs& A, int64_t v, double gx, double gy,
+                                           double& acc) {
+  const double2 pb = *reinterpret_cast<const double2*>(A.epi.pb + v);
+  const double2 pz = *reinterpret_cast<const double2*>(A.epi.pz + v);
+  const double2 s1 = *reinterpret_cast<const double2*>(A.epi.sig1 + v);
+  const double2 s2 = *reinterpret_cast<const double2*>(A.epi.sig2 + v);
+  double2 top, bot;
+  {
+    const double l1 = add(s1.x, s2.x), l2 = sub(s1.x, s2.x);
+    top.x = add(add(gx, mul(l1, pb.x)), mul(l2, pz.x));
+    bot.x = add(mul(l2, pb.x), mul(l1, pz.x));
+  }
+  {
+    const double l1 = add(s1.y, s2.y), l2 = sub(s1.y, s2.y);
+    top.y = add(add(gy, mul(l1, pb.y)), mul(l2, pz.y));
+    bot.y = add(mul(l2, pb.y), mul(l1, pz.y));
+  }
+  *reinterpret_cast<double2*>(A.out + v) = top;
+  if (A.epi.bottom) *reinterpret_cast<double2*>(A.epi.bottom + v) = bot;
+  acc += pb.x * top.x + pz.x * bot.x + pb.y * top.y + pz.y * bot.y;
+}
+
+// Raw input tile staging: element (k, fibre c) of the tile.
+template <int M, bool STRIDED>
+__device__ __forceinline__ int stage_idx(int k, int c) {
+  return STRIDED ? k * Geom<M>::W + c : c * M + k;
+}
+
+// Issue this thread's cp.async copies of tile ``tile`` (its natural-layout
+// elements k = q + r P of fibre c) into ``st``.
+template <int M, bool STRIDED>
+__device__ __forceinline__ void issue_tile(const PassArgs& A, int64_t tile, double2* st, int c, int q) {
+  using G = Geom<M>;
+  const int64_t g = tile * G::W + c;
+  if (g >= A.G) return;
+  const Geo Q = geo<STRIDED>(A, g);
+#pragma unroll
+  for (int r = 0; r < G::E; ++r) {
+    const int k = q + r * G::P;
+    double2* dst = st + stage_idx<M, STRIDED>(k, c);
+    if (STRIDED) {
+      cp_async16(dst, A.in + Q.bx + k * Q.st);
+    } else {
+      cp_async8(&dst->x, A.in + Q.bx + k);
+      if (Q.by >= 0) cp_async8(&dst->y, A.in + Q.by + k);
+    }
+  }
+}
+
+// Element (k, c) of the current raw tile: from staging (pipelined) or global.
+template <int M, bool STRIDED, bool PIPE>
+__device__ __forceinline__ double2 raw(const PassArgs& A, const double2* st, const Geo& Q, bool valid,
+                                       int k, int c) {
+  double2 z = make_double2(0.0, 0.0);
+  if (!valid) return z;
+  if (PIPE) {
+    z = st[stage_idx<M, STRIDED>(k, c)];
+    if (!STRIDED && Q.by < 0) z.y = 0.0;
+  } else if (STRIDED) {
+    z = *reinterpret_cast<const double2*>(A.in + Q.bx + (int64_t)k * Q.st);
+  } else {
+    z.x = A.in[Q.bx + k];
+    if (Q.by >= 0) z.y = A.in[Q.by + k];
+  }
+  return z;
+}
+
 template <int M, bool STRIDED, int KIND, bool EPI>
-__global__ void __launch_bounds__(Geom<M>::T, (KIND == K_GRAM || KIND == K_RESID) ? 1 : Geom<M>::MINB) fast_pass(const PassArgs A) {
+__global__ void __launch_bounds__(Geom<M>::T, Geom<M>::MINB) fast_pass(const PassArgs A) {
   using G = Geom<M>;
   constexpr int E = G::E, P = G::P, W = G::W, H = M / 2;
+  constexpr bool PIPE = G::PIPE;
   extern __shared__ double2 smem[];
   __shared__ double red[32];
   int c, q;
   lane_map<STRIDED>(threadIdx.x, W, P, c, q);
   double2* fib = smem + c * G::FS;
+  double2* stage0 = smem + G::FIB_BYTES / 16;
+  double2* stage1 = stage0 + W * M;
   const double2* tw = A.plan.tw;
   const double c0 = A.c0, c1 = A.c1;
   double acc = 0.0;
   const int64_t ntiles = (A.G + W - 1) / W;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  if (PIPE) {
+    if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED>(A, blockIdx.x, stage0, c, q);
+    cp_commit();
+  }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int64_t g = tile * W + c;
     const bool valid = g < A.G;
     const Geo Q = geo<STRIDED>(A, valid ? g : 0);
+    const double2* st = (it & 1) ? stage1 : stage0;
+    if (PIPE) {
+      const int64_t next = tile + gridDim.x;
+      if (next < ntiles) issue_tile<M, STRIDED>(A, next, (it & 1) ? stage0 : stage1, c, q);
+      cp_commit();
+      cp_wait<1>();
+      __syncthreads();
+    }
     double2 v[E];
     if (KIND == K_ANALYZE) {
 #pragma unroll
-      for (int r = 0; r < E; ++r) {
-        const int t = q + r * P;
-        double2 z = make_double2(0.0, 0.0);
-        if (valid) {
-          if (STRIDED) z = *reinterpret_cast<const double2*>(A.in + Q.bx + t * Q.st);
-          else {
-            z.x = A.in[Q.bx + t];
-            if (Q.by >= 0) z.y = A.in[Q.by + t];
-          }
-        }
-        v[r] = z;
-      }
+      for (int r = 0; r < E; ++r) v[r] = raw<M, STRIDED, PIPE>(A, st, Q, valid, q + r * P, c);
       fast::fft<M>(v, fib, q, tw, -1);
     } else {
       // unpack packed rows (j+1, j+h) into the combined half spectra Zin_j, Zin_{M-j}
 #pragma unroll
       for (int r = 0; r < E / 2; ++r) {
         const int j = q + r * P;
-        const int64_t ia = Q.st * (j ? j + 1 : 0), ib = Q.st * (j ? j + H : 1);
-        double xa = 0.0, xb = 0.0, ya = 0.0, yb = 0.0;
-        if (valid) {
-          if (STRIDED) {
-            const double2 a = *reinterpret_cast<const double2*>(A.in + Q.bx + ia);
-            const double2 b = *reinterpret_cast<const double2*>(A.in + Q.bx + ib);
-            xa = a.x; ya = a.y; xb = b.x; yb = b.y;
-          } else {
-            xa = A.in[Q.bx + ia];
-            xb = A.in[Q.bx + ib];
-            if (Q.by >= 0) { ya = A.in[Q.by + ia]; yb = A.in[Q.by + ib]; }
-          }
-        }
+        const double2 a = raw<M, STRIDED, PIPE>(A, st, Q, valid, j ? j + 1 : 0, c);
+        const double2 b = raw<M, STRIDED, PIPE>(A, st, Q, valid, j ? j + H : 1, c);
+        const double xa = a.x, ya = a.y, xb = b.x, yb = b.y;
         if (j == 0) {
           fib[si(0)] = make_double2(c0 * xa, c0 * ya);
           fib[si(H)] = make_double2(c0 * xb, c0 * yb);
@@ -100,7 +167,7 @@ __global__ void __launch_bounds__(Geom<M>::T, (KIND == K_GRAM || KIND == K_RESID
 #pragma unroll
           for (int r = 0; r < E; ++r) {
             const int t = q + r * P;
-            if (STRIDED) *reinterpret_cast<double2*>(A.out + Q.bx + t * Q.st) = v[r];
+            if (STRIDED) *reinterpret_cast<double2*>(A.out + Q.bx + (int64_t)t * Q.st) = v[r];
             else {
               A.out[Q.bx + t] = v[r].x;
               if (Q.by >= 0) A.out[Q.by + t] = v[r].y;
@@ -153,6 +220,9 @@ __global__ void __launch_bounds__(Geom<M>::T, (KIND == K_GRAM || KIND == K_RESID
           if (STRIDED && !EPI) {
             *reinterpret_cast<double2*>(A.out + Q.bx + ia) = make_double2(xa, ya);
             *reinterpret_cast<double2*>(A.out + Q.bx + ib) = make_double2(xb, yb);
+          } else if (STRIDED) {
+            kkt_store2(A, Q.bx + ia, xa, ya, acc);
+            kkt_store2(A, Q.bx + ib, xb, yb, acc);
           } else {
             put<STRIDED, EPI>(A, Q.bx + ia, xa, acc);
             put<STRIDED, EPI>(A, Q.bx + ib, xb, acc);
@@ -166,6 +236,7 @@ __global__ void __launch_bounds__(Geom<M>::T, (KIND == K_GRAM || KIND == K_RESID
     }
     __syncthreads();
   }
+  if (PIPE) cp_wait<0>();
   if (EPI && A.epi.partials) {
     const double s = block_reduce(acc, SumOp(), red);
     if (threadIdx.x == 0) A.epi.partials[blockIdx.x] = s;
@@ -245,7 +316,7 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
   if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");
   int& grid_cap = cache[lg][strided][kind][epi];
   if (!grid_cap) FL_TRY(grid_of(e, &grid_cap));
-  const int W = e.threads / (m / (m >= 1024 ? 16 : 8));
+  const int W = e.threads / (m / (m >= 1024 ? 16 : 8));  // == Geom<m>::W
   const int64_t tiles = (A.G + W - 1) / W;
   const int grid = (int)std::min<int64_t>(tiles, grid_cap);
   e.fn<<<grid, e.threads, e.smem, s>>>(A);
