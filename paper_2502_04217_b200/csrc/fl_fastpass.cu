@@ -60,23 +60,23 @@ __device__ __forceinline__ void kkt_store2(const PassArgs& A, int64_t v, double 
 }
 
 // Raw input tile staging: element (k, fibre c) of the tile.
-template <int M, bool STRIDED>
+template <int M, bool STRIDED, bool BIG>
 __device__ __forceinline__ int stage_idx(int k, int c) {
-  return STRIDED ? k * Geom<M>::W + c : c * M + k;
+  return STRIDED ? k * Geom<M, BIG>::W + c : c * M + k;
 }
 
 // Issue this thread's cp.async copies of tile ``tile`` (its natural-layout
 // elements k = q + r P of fibre c) into ``st``.
-template <int M, bool STRIDED>
+template <int M, bool STRIDED, bool BIG>
 __device__ __forceinline__ void issue_tile(const PassArgs& A, int64_t tile, double2* st, int c, int q) {
-  using G = Geom<M>;
+  using G = Geom<M, BIG>;
   const int64_t g = tile * G::W + c;
   if (g >= A.G) return;
   const Geo Q = geo<STRIDED>(A, g);
 #pragma unroll
   for (int r = 0; r < G::E; ++r) {
     const int k = q + r * G::P;
-    double2* dst = st + stage_idx<M, STRIDED>(k, c);
+    double2* dst = st + stage_idx<M, STRIDED, BIG>(k, c);
     if (STRIDED) {
       cp_async16(dst, A.in + Q.bx + k * Q.st);
     } else {
@@ -87,13 +87,13 @@ __device__ __forceinline__ void issue_tile(const PassArgs& A, int64_t tile, doub
 }
 
 // Element (k, c) of the current raw tile: from staging (pipelined) or global.
-template <int M, bool STRIDED, bool PIPE>
+template <int M, bool STRIDED, bool PIPE, bool BIG>
 __device__ __forceinline__ double2 raw(const PassArgs& A, const double2* st, const Geo& Q, bool valid,
                                        int k, int c) {
   double2 z = make_double2(0.0, 0.0);
   if (!valid) return z;
   if (PIPE) {
-    z = st[stage_idx<M, STRIDED>(k, c)];
+    z = st[stage_idx<M, STRIDED, BIG>(k, c)];
     if (!STRIDED && Q.by < 0) z.y = 0.0;
   } else if (STRIDED) {
     z = *reinterpret_cast<const double2*>(A.in + Q.bx + (int64_t)k * Q.st);
@@ -104,9 +104,9 @@ __device__ __forceinline__ double2 raw(const PassArgs& A, const double2* st, con
   return z;
 }
 
-template <int M, bool STRIDED, int KIND, bool EPI>
-__global__ void __launch_bounds__(Geom<M>::T, Geom<M>::MINB) fast_pass(const PassArgs A) {
-  using G = Geom<M>;
+template <int M, bool STRIDED, int KIND, bool EPI, bool BIG>
+__global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass(const PassArgs A) {
+  using G = Geom<M, BIG>;
   constexpr int E = G::E, P = G::P, W = G::W, H = M / 2;
   constexpr bool PIPE = G::PIPE;
   extern __shared__ double2 smem[];
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(Geom<M>::T, Geom<M>::MINB) fast_pass(const Pas
   double acc = 0.0;
   const int64_t ntiles = (A.G + W - 1) / W;
   if (PIPE) {
-    if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED>(A, blockIdx.x, stage0, c, q);
+    if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, BIG>(A, blockIdx.x, stage0, c, q);
     cp_commit();
   }
   int it = 0;
@@ -132,45 +132,68 @@ __global__ void __launch_bounds__(Geom<M>::T, Geom<M>::MINB) fast_pass(const Pas
     const double2* st = (it & 1) ? stage1 : stage0;
     if (PIPE) {
       const int64_t next = tile + gridDim.x;
-      if (next < ntiles) issue_tile<M, STRIDED>(A, next, (it & 1) ? stage0 : stage1, c, q);
+      if (next < ntiles) issue_tile<M, STRIDED, BIG>(A, next, (it & 1) ? stage0 : stage1, c, q);
       cp_commit();
       cp_wait<1>();
       __syncthreads();
     }
     double2 v[E];
     if (KIND == K_ANALYZE) {
+      if (PIPE) {
 #pragma unroll
-      for (int r = 0; r < E; ++r) v[r] = raw<M, STRIDED, PIPE>(A, st, Q, valid, q + r * P, c);
-      fast::fft<M>(v, fib, q, tw, -1);
+        for (int r = 0; r < E; ++r) v[r] = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, q + r * P, c);
+      } else {
+        // base pointer of row q, rows advance by P*st (no per-element 64-bit multiplies)
+        const double* px = A.in + Q.bx + (int64_t)q * Q.st;
+        const double* py = A.in + Q.by + (int64_t)q * Q.st;
+        const int64_t rs = (int64_t)P * Q.st;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          double2 z = make_double2(0.0, 0.0);
+          if (valid) {
+            if (STRIDED) z = *reinterpret_cast<const double2*>(px + r * rs);
+            else {
+              z.x = px[r * rs];
+              if (Q.by >= 0) z.y = py[r * rs];
+            }
+          }
+          v[r] = z;
+        }
+      }
+      fast::fft<M, BIG>(v, fib, q, tw, -1);
     } else {
       // unpack packed rows (j+1, j+h) into the combined half spectra Zin_j, Zin_{M-j}
+      const int qm = -q + ((-q) >> 3);
 #pragma unroll
       for (int r = 0; r < E / 2; ++r) {
         const int j = q + r * P;
-        const double2 a = raw<M, STRIDED, PIPE>(A, st, Q, valid, j ? j + 1 : 0, c);
-        const double2 b = raw<M, STRIDED, PIPE>(A, st, Q, valid, j ? j + H : 1, c);
+        const bool j0 = r == 0 && q == 0;
+        const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j0 ? 0 : j + 1, c);
+        const double2 b = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j0 ? 1 : j + H, c);
         const double xa = a.x, ya = a.y, xb = b.x, yb = b.y;
-        if (j == 0) {
-          fib[si(0)] = make_double2(c0 * xa, c0 * ya);
+        if (j0) {
+          fib[0] = make_double2(c0 * xa, c0 * ya);
           fib[si(H)] = make_double2(c0 * xb, c0 * yb);
         } else {
-          fib[si(j)] = make_double2(c1 * (xa - yb), c1 * (xb + ya));
-          fib[si(M - j)] = make_double2(c1 * (xa + yb), c1 * (ya - xb));
+          fib[fast::lo_idx<M, BIG>(q, r)] = make_double2(c1 * (xa - yb), c1 * (xb + ya));
+          fib[fast::hi_idx<M, BIG>(q, qm, r)] = make_double2(c1 * (xa + yb), c1 * (ya - xb));
         }
       }
       __syncthreads();
-      fast::load_natural<M>(v, fib, q);
+      fast::load_natural<M, BIG>(v, fib, q);
       __syncthreads();
-      fast::fft<M>(v, fib, q, tw, +1);
+      fast::fft<M, BIG>(v, fib, q, tw, +1);
       if (KIND == K_SYNTH) {
         if (valid) {
+          double* px = A.out + Q.bx + (int64_t)q * Q.st;
+          double* py = A.out + Q.by + (int64_t)q * Q.st;
+          const int64_t rs = (int64_t)P * Q.st;
 #pragma unroll
           for (int r = 0; r < E; ++r) {
-            const int t = q + r * P;
-            if (STRIDED) *reinterpret_cast<double2*>(A.out + Q.bx + (int64_t)t * Q.st) = v[r];
+            if (STRIDED) *reinterpret_cast<double2*>(px + r * rs) = v[r];
             else {
-              A.out[Q.bx + t] = v[r].x;
-              if (Q.by >= 0) A.out[Q.by + t] = v[r].y;
+              px[r * rs] = v[r].x;
+              if (Q.by >= 0) py[r * rs] = v[r].y;
             }
           }
         }
@@ -194,29 +217,31 @@ __global__ void __launch_bounds__(Geom<M>::T, Geom<M>::MINB) fast_pass(const Pas
           }
           v[r] = z;
         }
-        fast::fft<M>(v, fib, q, tw, -1);
+        fast::fft<M, BIG>(v, fib, q, tw, -1);
       }
     }
     if (KIND != K_SYNTH) {
-      fast::store_natural<M>(v, fib, q);
+      fast::store_natural<M, BIG>(v, fib, q);
       __syncthreads();
       if (valid) {
+        const int qm = -q + ((-q) >> 3);
 #pragma unroll
         for (int r = 0; r < E / 2; ++r) {
           const int j = q + r * P;
+          const bool j0 = r == 0 && q == 0;
           double xa, xb, ya, yb;
-          if (j == 0) {
-            const double2 z0 = fib[si(0)], zh = fib[si(H)];
+          if (j0) {
+            const double2 z0 = fib[0], zh = fib[si(H)];
             xa = c0 * z0.x; ya = c0 * z0.y;
             xb = c0 * zh.x; yb = c0 * zh.y;
           } else {
-            const double2 a = fib[si(j)], b = fib[si(M - j)];
+            const double2 a = fib[fast::lo_idx<M, BIG>(q, r)], b = fib[fast::hi_idx<M, BIG>(q, qm, r)];
             xa = c1 * (a.x + b.x);
             xb = c1 * (a.y - b.y);
             ya = c1 * (a.y + b.y);
             yb = c1 * (b.x - a.x);
           }
-          const int64_t ia = Q.st * (j ? j + 1 : 0), ib = Q.st * (j ? j + H : 1);
+          const int64_t ia = Q.st * (j0 ? 0 : j + 1), ib = Q.st * (j0 ? 1 : j + H);
           if (STRIDED && !EPI) {
             *reinterpret_cast<double2*>(A.out + Q.bx + ia) = make_double2(xa, ya);
             *reinterpret_cast<double2*>(A.out + Q.bx + ib) = make_double2(xb, yb);
@@ -245,25 +270,44 @@ __global__ void __launch_bounds__(Geom<M>::T, Geom<M>::MINB) fast_pass(const Pas
 
 struct Entry {
   KernelFn fn = nullptr;
-  int threads = 0, smem = 0, grid = 0;
+  int threads = 0, smem = 0, w = 0;
 };
 
 template <int M, bool S>
 Entry make(int kind, bool epi) {
   Entry e;
-  using G = Geom<M>;
+  // plain strided passes: big CTAs; gram / epilogue passes: pipelined small CTAs
+  constexpr bool BIG_OK = M <= 512;
+  const bool big = BIG_OK && S && !epi && (kind == K_SYNTH || kind == K_ANALYZE);
+  if (big) {
+    if constexpr (BIG_OK && S) {
+      using G = Geom<M, true>;
+      e.fn = kind == K_SYNTH ? fast_pass<M, true, K_SYNTH, false, true>
+                             : fast_pass<M, true, K_ANALYZE, false, true>;
+      e.threads = G::T;
+      e.smem = G::SMEM;
+      e.w = G::W;
+    }
+    return e;
+  }
+  using G = Geom<M, false>;
   switch (kind) {
-    case K_SYNTH: e.fn = fast_pass<M, S, K_SYNTH, false>; break;
-    case K_ANALYZE: e.fn = epi ? fast_pass<M, S, K_ANALYZE, true> : fast_pass<M, S, K_ANALYZE, false>; break;
+    case K_SYNTH: e.fn = fast_pass<M, S, K_SYNTH, false, false>; break;
+    case K_ANALYZE:
+      e.fn = epi ? fast_pass<M, S, K_ANALYZE, true, false> : fast_pass<M, S, K_ANALYZE, false, false>;
+      break;
     case K_GRAM:
-      if constexpr (!S) e.fn = epi ? fast_pass<M, false, K_GRAM, true> : fast_pass<M, false, K_GRAM, false>;
+      if constexpr (!S)
+        e.fn = epi ? fast_pass<M, false, K_GRAM, true, false> : fast_pass<M, false, K_GRAM, false, false>;
       break;
     default:
-      if constexpr (!S) e.fn = epi ? fast_pass<M, false, K_RESID, true> : fast_pass<M, false, K_RESID, false>;
+      if constexpr (!S)
+        e.fn = epi ? fast_pass<M, false, K_RESID, true, false> : fast_pass<M, false, K_RESID, false, false>;
       break;
   }
   e.threads = G::T;
   e.smem = G::SMEM;
+  e.w = G::W;
   return e;
 }
 
@@ -316,8 +360,7 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
   if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");
   int& grid_cap = cache[lg][strided][kind][epi];
   if (!grid_cap) FL_TRY(grid_of(e, &grid_cap));
-  const int W = e.threads / (m / (m >= 1024 ? 16 : 8));  // == Geom<m>::W
-  const int64_t tiles = (A.G + W - 1) / W;
+  const int64_t tiles = (A.G + e.w - 1) / e.w;
   const int grid = (int)std::min<int64_t>(tiles, grid_cap);
   e.fn<<<grid, e.threads, e.smem, s>>>(A);
   FL_LAUNCH_CHECK();

@@ -32,7 +32,15 @@ __device__ __forceinline__ Geo geo(const PassArgs& A, int64_t g) {
   Geo r;
   if (STRIDED) {
     const int64_t ppo = A.inner >> 1;
-    const int64_t o = g / ppo, q = g - o * ppo;
+    int64_t o, q;
+    if (A.G <= 0xffffffffLL) {  // 32-bit division (all single-GPU grid sizes)
+      const unsigned o32 = (unsigned)g / (unsigned)ppo;
+      o = o32;
+      q = g - (int64_t)o32 * ppo;
+    } else {
+      o = g / ppo;
+      q = g - o * ppo;
+    }
     r.bx = o * (int64_t)A.m * A.inner + 2 * q;
     r.by = r.bx + 1;
     r.st = A.inner;
