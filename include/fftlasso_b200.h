@@ -138,7 +138,8 @@ FL_API int fl_kkt_apply(fl_plan_t plan, const uint32_t* miss_bits, const double*
                  const double* sigma2, const double* d_beta, const double* d_z, double* top,
                  double* bottom, double* pkp_host, fl_stream_t stream);
 /* fl_kkt_apply with a cudaEvent after every HBM pass; writes the per-pass
- * device times (ms) to ``pass_ms`` (host, 2*ndim-1 entries) and returns the
+ * device times (ms) to ``pass_ms`` (host, 2*ndim entries: 2*ndim-1 transform
+ * passes + the elementwise KKT epilogue) and returns the
  * number of passes in ``npasses``.  Measurement hook for bench.py. */
 FL_API int fl_kkt_apply_profiled(fl_plan_t plan, const uint32_t* miss_bits, const double* sigma1,
                                  const double* sigma2, const double* d_beta, const double* d_z,

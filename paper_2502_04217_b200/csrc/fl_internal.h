@@ -57,6 +57,10 @@ int op_analyze(const fl_plan* p, const double* in, double* out, cudaStream_t s);
 int op_gram(const fl_plan* p, const uint32_t* bits, const double* bhat, bool resid,
             const double* in, double* out, const KktEpi* epi, int* nblocks, cudaStream_t s);
 
+// Elementwise KKT epilogue on a gram output (fl_vec.cu); n even.
+int kkt_epilogue(int64_t n, double* g, const double* pb, const double* pz, const double* sig1,
+                 const double* sig2, double* bottom, double* partials, int* nblocks, cudaStream_t s);
+
 // PCG kernels (fl_vec.cu)
 int pcg_init(int64_t n, const double* sig1, const double* sig2, const double* rhs, double* x,
              double* r, double* p, double* partials, int* nblocks, cudaStream_t s);

@@ -312,8 +312,24 @@ int op_analyze(const fl_plan* p, const double* in, double* out, cudaStream_t s) 
   return FL_OK;
 }
 
+// The KKT epilogue runs fused into the last pass's store (FL_FUSED_EPI=1) or,
+// by default, as a separate 16-byte elementwise pass: its four operand
+// streams then load at full bandwidth instead of after the tile's FFT.
+static bool fused_epilogue() {
+  static const bool on = [] {
+    const char* e = std::getenv("FL_FUSED_EPI");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int op_gram(const fl_plan* p, const uint32_t* bits, const double* bhat, bool resid,
             const double* in, double* out, const KktEpi* epi, int* nblocks, cudaStream_t s) {
+  if (epi && !fused_epilogue() && p->n % 2 == 0) {
+    FL_TRY(op_gram(p, bits, bhat, resid, in, out, nullptr, nullptr, s));
+    return kkt_epilogue(p->n, out, epi->pb, epi->pz, epi->sig1, epi->sig2, epi->bottom, epi->partials,
+                        nblocks, s);
+  }
   const int d = p->ndim;
   const int mid = resid ? K_RESID : K_GRAM;
   if (d == 1) return run_pass(p, 0, mid, in, out, bits, bhat, epi, nblocks, s);

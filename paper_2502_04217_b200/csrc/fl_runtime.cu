@@ -259,21 +259,15 @@ int fl_kkt_apply_profiled(fl_plan_t p, const uint32_t* bits, const double* sigma
   if (!p || !bits || !sigma1 || !sigma2 || !d_beta || !d_z || !top || !pass_ms || !npasses)
     return fail(FL_E_VALUE, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
-  KktEpi e;
-  e.pb = d_beta;
-  e.pz = d_z;
-  e.sig1 = sigma1;
-  e.sig2 = sigma2;
-  e.bottom = bottom;
   const int d = p->ndim;
-  const int np = 2 * d - 1;
+  const int np = 2 * d;  // 2d-1 transform passes + the elementwise epilogue
   cudaEvent_t ev[8];
   for (int i = 0; i <= np; ++i) FL_CUDA(cudaEventCreate(&ev[i]));
   int st = FL_OK;
   FL_CUDA(cudaEventRecord(ev[0], s));
   int k = 0;
   if (d == 1) {
-    st = run_pass(p, 0, K_GRAM, d_beta, top, bits, nullptr, &e, nullptr, s);
+    st = run_pass(p, 0, K_GRAM, d_beta, top, bits, nullptr, nullptr, nullptr, s);
     cudaEventRecord(ev[++k], s);
   } else {
     const double* src = d_beta;
@@ -285,10 +279,12 @@ int fl_kkt_apply_profiled(fl_plan_t p, const uint32_t* bits, const double* sigma
     if (st == FL_OK) st = run_pass(p, d - 1, K_GRAM, top, top, bits, nullptr, nullptr, nullptr, s);
     cudaEventRecord(ev[++k], s);
     for (int a = d - 2; a >= 0 && st == FL_OK; --a) {
-      st = run_pass(p, a, K_ANALYZE, top, top, nullptr, nullptr, a == 0 ? &e : nullptr, nullptr, s);
+      st = run_pass(p, a, K_ANALYZE, top, top, nullptr, nullptr, nullptr, nullptr, s);
       cudaEventRecord(ev[++k], s);
     }
   }
+  if (st == FL_OK) st = kkt_epilogue(p->n, top, d_beta, d_z, sigma1, sigma2, bottom, nullptr, nullptr, s);
+  cudaEventRecord(ev[++k], s);
   if (st == FL_OK) {
     FL_CUDA(cudaEventSynchronize(ev[np]));
     for (int i = 0; i < np; ++i) {

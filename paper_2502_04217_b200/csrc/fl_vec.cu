@@ -465,6 +465,32 @@ __global__ void k_pcg_pupdate(int64_t n, const double* __restrict__ g1, const do
   }
 }
 
+// KKT epilogue (newton_system.py:150-151) on the gram output g, in place:
+// top = (g + L1 pb) + L2 pz, bottom = L2 pb + L1 pz, partial d.Kd.  16-byte
+// accesses (n is even for every grid).
+__global__ void k_kkt_epilogue(int64_t n2, double2* __restrict__ g, const double2* __restrict__ pb,
+                               const double2* __restrict__ pz, const double2* __restrict__ s1,
+                               const double2* __restrict__ s2, double2* __restrict__ bot,
+                               double* __restrict__ partials) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  GRID_LOOP(i, n2) {
+    const double2 gv = g[i], b = pb[i], z = pz[i], a1 = s1[i], a2 = s2[i];
+    double2 t, u;
+    double l1 = add(a1.x, a2.x), l2 = sub(a1.x, a2.x);
+    t.x = add(add(gv.x, mul(l1, b.x)), mul(l2, z.x));
+    u.x = add(mul(l2, b.x), mul(l1, z.x));
+    l1 = add(a1.y, a2.y);
+    l2 = sub(a1.y, a2.y);
+    t.y = add(add(gv.y, mul(l1, b.y)), mul(l2, z.y));
+    u.y = add(mul(l2, b.y), mul(l1, z.y));
+    g[i] = t;
+    if (bot) bot[i] = u;
+    acc += mul(b.x, t.x) + mul(z.x, u.x) + mul(b.y, t.y) + mul(z.y, u.y);
+  }
+  if (partials) emit(acc, SumOp(), red, partials, 0);
+}
+
 // Reduce ``nk`` partial rows and fetch them to the host.
 int reduce_fetch(Scratch* sc, int grid, int nk, const int* kinds, double* out, cudaStream_t s) {
   FL_TRY(finish_reduce(sc->partials, grid, nk, kinds, sc->result, s));
@@ -492,6 +518,19 @@ int pcg_update(int64_t n, const double* sig1, const double* sig2, const double* 
   k_pcg_update<<<grid, T, 0, s>>>(n, sig1, sig2, rho, curv, x, r, p, kp_top, kp_bot, partials);
   FL_LAUNCH_CHECK();
   *nblocks = grid;
+  return FL_OK;
+}
+
+int kkt_epilogue(int64_t n, double* g, const double* pb, const double* pz, const double* sig1,
+                 const double* sig2, double* bottom, double* partials, int* nblocks, cudaStream_t s) {
+  const int64_t n2 = n / 2;
+  const int grid = grid_for(n2, T, 148 * 16);
+  k_kkt_epilogue<<<grid, T, 0, s>>>(n2, reinterpret_cast<double2*>(g), reinterpret_cast<const double2*>(pb),
+                                    reinterpret_cast<const double2*>(pz), reinterpret_cast<const double2*>(sig1),
+                                    reinterpret_cast<const double2*>(sig2), reinterpret_cast<double2*>(bottom),
+                                    partials);
+  FL_LAUNCH_CHECK();
+  if (nblocks) *nblocks = grid;
   return FL_OK;
 }
 
