@@ -162,26 +162,69 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
       }
       fast::fft<M, BIG>(v, fib, q, tw, -1);
     } else {
-      // unpack packed rows (j+1, j+h) into the combined half spectra Zin_j, Zin_{M-j}
-      const int qm = -q + ((-q) >> 3);
+      if constexpr (PIPE) {
+        // unpack straight from the staged raw rows into the natural layout:
+        // Zin_k needs rows (k+1, k+h) for k < h and rows (M-k+1, M-k+h) above h
 #pragma unroll
-      for (int r = 0; r < E / 2; ++r) {
-        const int j = q + r * P;
-        const bool j0 = r == 0 && q == 0;
-        const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j0 ? 0 : j + 1, c);
-        const double2 b = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j0 ? 1 : j + H, c);
-        const double xa = a.x, ya = a.y, xb = b.x, yb = b.y;
-        if (j0) {
-          fib[0] = make_double2(c0 * xa, c0 * ya);
-          fib[si(H)] = make_double2(c0 * xb, c0 * yb);
-        } else {
-          fib[fast::lo_idx<M, BIG>(q, r)] = make_double2(c1 * (xa - yb), c1 * (xb + ya));
-          fib[fast::hi_idx<M, BIG>(q, qm, r)] = make_double2(c1 * (xa + yb), c1 * (ya - xb));
+        for (int r = 0; r < E; ++r) {
+          const int k = q + r * P;
+          double2 z;
+          if (r < E / 2) {
+            if (r == 0 && q == 0) {
+              const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, 0, c);
+              z = make_double2(c0 * a.x, c0 * a.y);
+            } else {
+              const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, k + 1, c);
+              const double2 b = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, k + H, c);
+              z = make_double2(c1 * (a.x - b.y), c1 * (b.x + a.y));
+            }
+          } else {
+            if (r == E / 2 && q == 0) {
+              const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, 1, c);
+              z = make_double2(c0 * a.x, c0 * a.y);
+            } else {
+              const int j = M - k;
+              const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j + 1, c);
+              const double2 b = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j + H, c);
+              z = make_double2(c1 * (a.x + b.y), c1 * (a.y - b.x));
+            }
+          }
+          v[r] = z;
+        }
+      } else {
+        // unpack packed rows (j+1, j+h) into the combined half spectra Zin_j, Zin_{M-j}
+        const int qm = -q + ((-q) >> 3);
+  #pragma unroll
+        for (int r = 0; r < E / 2; ++r) {
+          const int j = q + r * P;
+          const bool j0 = r == 0 && q == 0;
+          const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j0 ? 0 : j + 1, c);
+          const double2 b = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j0 ? 1 : j + H, c);
+          const double xa = a.x, ya = a.y, xb = b.x, yb = b.y;
+          if (j0) {
+            fib[0] = make_double2(c0 * xa, c0 * ya);
+            fib[si(H)] = make_double2(c0 * xb, c0 * yb);
+          } else {
+            fib[fast::lo_idx<M, BIG>(q, r)] = make_double2(c1 * (xa - yb), c1 * (xb + ya));
+            fib[fast::hi_idx<M, BIG>(q, qm, r)] = make_double2(c1 * (xa + yb), c1 * (ya - xb));
+          }
+        }
+        __syncthreads();
+        fast::load_natural<M, BIG>(v, fib, q);
+        __syncthreads();
+      }
+      // mask words for this thread's samples, fetched before the inverse FFT so
+      // their latency hides behind it (one 32-bit word per sample, L1/L2 hits)
+      uint32_t wx[(KIND == K_GRAM || KIND == K_RESID) ? E : 1];
+      uint32_t wy[(KIND == K_GRAM || KIND == K_RESID) ? E : 1];
+      if constexpr (KIND == K_GRAM || KIND == K_RESID) {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int64_t vx = Q.bx + q + r * P;
+          wx[r] = valid ? __ldg(A.bits + (vx >> 5)) : 0u;
+          wy[r] = (valid && Q.by >= 0) ? __ldg(A.bits + ((Q.by + q + r * P) >> 5)) : 0u;
         }
       }
-      __syncthreads();
-      fast::load_natural<M, BIG>(v, fib, q);
-      __syncthreads();
       fast::fft<M, BIG>(v, fib, q, tw, +1);
       if (KIND == K_SYNTH) {
         if (valid) {
@@ -205,12 +248,14 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
           double2 z = v[r];
           if (valid) {
             const int64_t vx = Q.bx + t;
-            if (KIND == K_RESID) z.x = missing(A.bits, vx) ? 0.0 : A.bhat[vx] - z.x;
-            else if (missing(A.bits, vx)) z.x = 0.0;
+            const bool mx = (wx[r] >> (vx & 31)) & 1u;
+            if (KIND == K_RESID) z.x = mx ? 0.0 : A.bhat[vx] - z.x;
+            else if (mx) z.x = 0.0;
             if (Q.by >= 0) {
               const int64_t vy = Q.by + t;
-              if (KIND == K_RESID) z.y = missing(A.bits, vy) ? 0.0 : A.bhat[vy] - z.y;
-              else if (missing(A.bits, vy)) z.y = 0.0;
+              const bool my = (wy[r] >> (vy & 31)) & 1u;
+              if (KIND == K_RESID) z.y = my ? 0.0 : A.bhat[vy] - z.y;
+              else if (my) z.y = 0.0;
             } else {
               z.y = 0.0;
             }
