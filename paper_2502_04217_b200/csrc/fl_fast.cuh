@@ -27,23 +27,29 @@ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 constexpr int nfull(int m, int e) { return (m % e == 0 && m > 1) ? 1 + nfull(m / e, e) : 0; }
 constexpr int imax(int a, int b) { return a > b ? a : b; }
 
-// BIG: 512-thread CTAs, E elements per thread, no staging (2 CTAs/SM at 64
-// registers) -- best for the plain strided synthesis/analysis passes.
-// !BIG: 256-thread CTAs with cp.async double-buffered staging of the next
-// tile (2 CTAs/SM at 128 registers) -- best for the two-FFT gram pass and
-// the KKT-epilogue pass.
-template <int M, bool BIG = false>
+// CFG selects the CTA shape, input staging and residency target of a pass
+// kernel: CFG = cfg_code(T_SEL, PIPE, MB) with T_SEL 0 -> 256 threads,
+// 1 -> 512 threads, MB = CTAs per SM requested from __launch_bounds__, and
+//   PIPE 0 -> registers load straight from global (no staging),
+//        1 -> one cp.async staging buffer, refilled with the next tile as
+//             soon as the current tile has been read out of it,
+//        2 -> two staging buffers (double buffering).
+constexpr int cfg_code(int t_sel, int pipe, int mb) { return t_sel * 9 + pipe * 3 + (mb - 1); }
+
+template <int M, int CFG = 0>
 struct Geom {
   static constexpr int E = M >= 1024 ? 16 : 8;                  // elements per thread
   static constexpr int P = M / E;                               // threads per fibre
-  static constexpr int T = BIG ? imax(512, P) : imax(256, P);   // threads per CTA
+  static constexpr int T_SEL = CFG / 9;
+  static constexpr int PIPE_REQ = (CFG / 3) % 3;
+  static constexpr int MB = CFG % 3 + 1;
+  static constexpr int T = imax(T_SEL ? 512 : 256, P);          // threads per CTA
   static constexpr int W = T / P;                               // fibres per CTA tile
   static constexpr int FS = M + M / 8 + 1;                      // smem fibre stride (double2)
   static constexpr int FIB_BYTES = W * FS * 16;                 // exchange buffer
   static constexpr int STAGE_BYTES = W * M * 16;                // one raw input tile
-  static constexpr bool PIPE = !BIG && FIB_BYTES + 2 * STAGE_BYTES <= 113 * 1024;
-  static constexpr int SMEM = FIB_BYTES + (PIPE ? 2 * STAGE_BYTES : 0);
-  static constexpr int MINB = (PIPE || (BIG && M <= 512)) ? 2 : 1;  // resident CTAs targeted per SM
+  static constexpr int PIPE = FIB_BYTES + PIPE_REQ * STAGE_BYTES <= 220 * 1024 ? PIPE_REQ : 0;
+  static constexpr int SMEM = FIB_BYTES + PIPE * STAGE_BYTES;
   static constexpr int NFULL = nfull(M, E);
   static constexpr int REM = M / ipow(E, NFULL);                // first-stage radix if > 1
   static constexpr int NST = NFULL + (REM > 1 ? 1 : 0);
@@ -127,9 +133,9 @@ __device__ __forceinline__ void twiddles(double2* w, int j, const double2* tw, i
 }
 
 // One stage: butterflies of radix R on the natural-layout registers.
-template <int M, bool BIG, int S>
+template <int M, int CFG, int S>
 __device__ __forceinline__ void stage_compute(double2* v, int q, const double2* tw, int sign) {
-  using G = Geom<M, BIG>;
+  using G = Geom<M, CFG>;
   constexpr int R = G::radix(S), NS = G::ns(S), B = G::E / R, P = G::P;
 #pragma unroll
   for (int b = 0; b < B; ++b) {
@@ -147,9 +153,9 @@ __device__ __forceinline__ void stage_compute(double2* v, int q, const double2* 
 // Write stage S outputs to smem at their Stockham destinations.  The padded
 // index si(pos) is split into a per-butterfly base plus compile-time offsets
 // wherever the stage geometry allows it (no per-element integer math).
-template <int M, bool BIG, int S>
+template <int M, int CFG, int S>
 __device__ __forceinline__ void stage_store(const double2* v, double2* fib, int q) {
-  using G = Geom<M, BIG>;
+  using G = Geom<M, CFG>;
   constexpr int R = G::radix(S), NS = G::ns(S), B = G::E / R, P = G::P;
 #pragma unroll
   for (int b = 0; b < B; ++b) {
@@ -173,9 +179,9 @@ __device__ __forceinline__ void stage_store(const double2* v, double2* fib, int 
 }
 
 // Natural layout: element q + r P.  For P % 8 == 0, si(q + r P) = si(q) + r (P + P/8).
-template <int M, bool BIG>
+template <int M, int CFG>
 __device__ __forceinline__ void load_natural(double2* v, const double2* fib, int q) {
-  using G = Geom<M, BIG>;
+  using G = Geom<M, CFG>;
   constexpr int P = G::P;
   if constexpr (P % 8 == 0) {
     const double2* o = fib + si(q);
@@ -187,9 +193,9 @@ __device__ __forceinline__ void load_natural(double2* v, const double2* fib, int
   }
 }
 
-template <int M, bool BIG>
+template <int M, int CFG>
 __device__ __forceinline__ void store_natural(const double2* v, double2* fib, int q) {
-  using G = Geom<M, BIG>;
+  using G = Geom<M, CFG>;
   constexpr int P = G::P;
   if constexpr (P % 8 == 0) {
     double2* o = fib + si(q);
@@ -204,30 +210,30 @@ __device__ __forceinline__ void store_natural(const double2* v, double2* fib, in
 // si(j) and si(M - j) for j = q + r P (r < E/2): per-thread part + constants.
 // With a = M - r P (a multiple of 8 when P is): si(a - q) = a + a/8 + qm,
 // qm = -q + floor(-q / 8).
-template <int M, bool BIG>
+template <int M, int CFG>
 __device__ __forceinline__ int lo_idx(int q, int r) {
-  constexpr int P = Geom<M, BIG>::P;
+  constexpr int P = Geom<M, CFG>::P;
   if constexpr (P % 8 == 0) return si(q) + r * (P + P / 8);
   else return si(q + r * P);
 }
-template <int M, bool BIG>
+template <int M, int CFG>
 __device__ __forceinline__ int hi_idx(int q, int qm, int r) {
-  constexpr int P = Geom<M, BIG>::P;
+  constexpr int P = Geom<M, CFG>::P;
   if constexpr (P % 8 == 0) return (M - r * P) + (M - r * P) / 8 + qm;
   else return si(M - q - r * P);
 }
 
 // Full FFT from natural-layout registers to natural-layout registers.
-template <int M, bool BIG, int S = 0>
+template <int M, int CFG, int S = 0>
 __device__ __forceinline__ void fft(double2* v, double2* fib, int q, const double2* tw, int sign) {
-  using G = Geom<M, BIG>;
-  stage_compute<M, BIG, S>(v, q, tw, sign);
+  using G = Geom<M, CFG>;
+  stage_compute<M, CFG, S>(v, q, tw, sign);
   if constexpr (S + 1 < G::NST) {
-    stage_store<M, BIG, S>(v, fib, q);
+    stage_store<M, CFG, S>(v, fib, q);
     __syncthreads();
-    load_natural<M, BIG>(v, fib, q);
+    load_natural<M, CFG>(v, fib, q);
     __syncthreads();
-    fft<M, BIG, S + 1>(v, fib, q, tw, sign);
+    fft<M, CFG, S + 1>(v, fib, q, tw, sign);
   }
 }
 

@@ -13,6 +13,9 @@
 // A persistent grid (resident CTAs x 148 SMs) walks the tiles.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 
 #include "fl_common.cuh"
@@ -25,6 +28,7 @@ namespace {
 
 using fast::Geom;
 using fast::si;
+using fast::cfg_code;
 using fast::cp_async16;
 using fast::cp_async8;
 using fast::cp_commit;
@@ -60,23 +64,23 @@ __device__ __forceinline__ void kkt_store2(const PassArgs& A, int64_t v, double 
 }
 
 // Raw input tile staging: element (k, fibre c) of the tile.
-template <int M, bool STRIDED, bool BIG>
+template <int M, bool STRIDED, int CFG>
 __device__ __forceinline__ int stage_idx(int k, int c) {
-  return STRIDED ? k * Geom<M, BIG>::W + c : c * M + k;
+  return STRIDED ? k * Geom<M, CFG>::W + c : c * M + k;
 }
 
 // Issue this thread's cp.async copies of tile ``tile`` (its natural-layout
 // elements k = q + r P of fibre c) into ``st``.
-template <int M, bool STRIDED, bool BIG>
+template <int M, bool STRIDED, int CFG>
 __device__ __forceinline__ void issue_tile(const PassArgs& A, int64_t tile, double2* st, int c, int q) {
-  using G = Geom<M, BIG>;
+  using G = Geom<M, CFG>;
   const int64_t g = tile * G::W + c;
   if (g >= A.G) return;
   const Geo Q = geo<STRIDED>(A, g);
 #pragma unroll
   for (int r = 0; r < G::E; ++r) {
     const int k = q + r * G::P;
-    double2* dst = st + stage_idx<M, STRIDED, BIG>(k, c);
+    double2* dst = st + stage_idx<M, STRIDED, CFG>(k, c);
     if (STRIDED) {
       cp_async16(dst, A.in + Q.bx + k * Q.st);
     } else {
@@ -87,13 +91,13 @@ __device__ __forceinline__ void issue_tile(const PassArgs& A, int64_t tile, doub
 }
 
 // Element (k, c) of the current raw tile: from staging (pipelined) or global.
-template <int M, bool STRIDED, bool PIPE, bool BIG>
+template <int M, bool STRIDED, bool PIPE, int CFG>
 __device__ __forceinline__ double2 raw(const PassArgs& A, const double2* st, const Geo& Q, bool valid,
                                        int k, int c) {
   double2 z = make_double2(0.0, 0.0);
   if (!valid) return z;
   if (PIPE) {
-    z = st[stage_idx<M, STRIDED, BIG>(k, c)];
+    z = st[stage_idx<M, STRIDED, CFG>(k, c)];
     if (!STRIDED && Q.by < 0) z.y = 0.0;
   } else if (STRIDED) {
     z = *reinterpret_cast<const double2*>(A.in + Q.bx + (int64_t)k * Q.st);
@@ -104,9 +108,21 @@ __device__ __forceinline__ double2 raw(const PassArgs& A, const double2* st, con
   return z;
 }
 
-template <int M, bool STRIDED, int KIND, bool EPI, bool BIG>
-__global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass(const PassArgs A) {
-  using G = Geom<M, BIG>;
+// Single-buffer staging: once every thread has read the current tile out of
+// the stage, start copying the next tile into it (overlaps this tile's FFT).
+template <int M, bool STRIDED, int CFG>
+__device__ __forceinline__ void refill(const PassArgs& A, int64_t next, int64_t ntiles, double2* stage,
+                                       int c, int q) {
+  if constexpr (Geom<M, CFG>::PIPE == 1) {
+    __syncthreads();
+    if (next < ntiles) issue_tile<M, STRIDED, CFG>(A, next, stage, c, q);
+    cp_commit();
+  }
+}
+
+template <int M, bool STRIDED, int KIND, bool EPI, int CFG>
+__global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(const PassArgs A) {
+  using G = Geom<M, CFG>;
   constexpr int E = G::E, P = G::P, W = G::W, H = M / 2;
   constexpr bool PIPE = G::PIPE;
   extern __shared__ double2 smem[];
@@ -121,7 +137,7 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
   double acc = 0.0;
   const int64_t ntiles = (A.G + W - 1) / W;
   if (PIPE) {
-    if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, BIG>(A, blockIdx.x, stage0, c, q);
+    if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, CFG>(A, blockIdx.x, stage0, c, q);
     cp_commit();
   }
   int it = 0;
@@ -129,19 +145,23 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
     const int64_t g = tile * W + c;
     const bool valid = g < A.G;
     const Geo Q = geo<STRIDED>(A, valid ? g : 0);
-    const double2* st = (it & 1) ? stage1 : stage0;
-    if (PIPE) {
-      const int64_t next = tile + gridDim.x;
-      if (next < ntiles) issue_tile<M, STRIDED, BIG>(A, next, (it & 1) ? stage0 : stage1, c, q);
+    const int64_t next = tile + gridDim.x;
+    const double2* st = (PIPE == 2 && (it & 1)) ? stage1 : stage0;
+    if (PIPE == 2) {
+      if (next < ntiles) issue_tile<M, STRIDED, CFG>(A, next, (it & 1) ? stage0 : stage1, c, q);
       cp_commit();
       cp_wait<1>();
+      __syncthreads();
+    } else if (PIPE == 1) {
+      cp_wait<0>();
       __syncthreads();
     }
     double2 v[E];
     if (KIND == K_ANALYZE) {
       if (PIPE) {
 #pragma unroll
-        for (int r = 0; r < E; ++r) v[r] = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, q + r * P, c);
+        for (int r = 0; r < E; ++r) v[r] = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, q + r * P, c);
+        refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
       } else {
         // base pointer of row q, rows advance by P*st (no per-element 64-bit multiplies)
         const double* px = A.in + Q.bx + (int64_t)q * Q.st;
@@ -160,7 +180,7 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
           v[r] = z;
         }
       }
-      fast::fft<M, BIG>(v, fib, q, tw, -1);
+      fast::fft<M, CFG>(v, fib, q, tw, -1);
     } else {
       if constexpr (PIPE) {
         // unpack straight from the staged raw rows into the natural layout:
@@ -171,26 +191,27 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
           double2 z;
           if (r < E / 2) {
             if (r == 0 && q == 0) {
-              const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, 0, c);
+              const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, 0, c);
               z = make_double2(c0 * a.x, c0 * a.y);
             } else {
-              const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, k + 1, c);
-              const double2 b = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, k + H, c);
+              const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, k + 1, c);
+              const double2 b = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, k + H, c);
               z = make_double2(c1 * (a.x - b.y), c1 * (b.x + a.y));
             }
           } else {
             if (r == E / 2 && q == 0) {
-              const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, 1, c);
+              const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, 1, c);
               z = make_double2(c0 * a.x, c0 * a.y);
             } else {
               const int j = M - k;
-              const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j + 1, c);
-              const double2 b = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j + H, c);
+              const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, j + 1, c);
+              const double2 b = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, j + H, c);
               z = make_double2(c1 * (a.x + b.y), c1 * (a.y - b.x));
             }
           }
           v[r] = z;
         }
+        refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
       } else {
         // unpack packed rows (j+1, j+h) into the combined half spectra Zin_j, Zin_{M-j}
         const int qm = -q + ((-q) >> 3);
@@ -198,19 +219,19 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
         for (int r = 0; r < E / 2; ++r) {
           const int j = q + r * P;
           const bool j0 = r == 0 && q == 0;
-          const double2 a = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j0 ? 0 : j + 1, c);
-          const double2 b = raw<M, STRIDED, PIPE, BIG>(A, st, Q, valid, j0 ? 1 : j + H, c);
+          const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, j0 ? 0 : j + 1, c);
+          const double2 b = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, j0 ? 1 : j + H, c);
           const double xa = a.x, ya = a.y, xb = b.x, yb = b.y;
           if (j0) {
             fib[0] = make_double2(c0 * xa, c0 * ya);
             fib[si(H)] = make_double2(c0 * xb, c0 * yb);
           } else {
-            fib[fast::lo_idx<M, BIG>(q, r)] = make_double2(c1 * (xa - yb), c1 * (xb + ya));
-            fib[fast::hi_idx<M, BIG>(q, qm, r)] = make_double2(c1 * (xa + yb), c1 * (ya - xb));
+            fib[fast::lo_idx<M, CFG>(q, r)] = make_double2(c1 * (xa - yb), c1 * (xb + ya));
+            fib[fast::hi_idx<M, CFG>(q, qm, r)] = make_double2(c1 * (xa + yb), c1 * (ya - xb));
           }
         }
         __syncthreads();
-        fast::load_natural<M, BIG>(v, fib, q);
+        fast::load_natural<M, CFG>(v, fib, q);
         __syncthreads();
       }
       // mask words for this thread's samples, fetched before the inverse FFT so
@@ -225,7 +246,7 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
           wy[r] = (valid && Q.by >= 0) ? __ldg(A.bits + ((Q.by + q + r * P) >> 5)) : 0u;
         }
       }
-      fast::fft<M, BIG>(v, fib, q, tw, +1);
+      fast::fft<M, CFG>(v, fib, q, tw, +1);
       if (KIND == K_SYNTH) {
         if (valid) {
           double* px = A.out + Q.bx + (int64_t)q * Q.st;
@@ -262,11 +283,11 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
           }
           v[r] = z;
         }
-        fast::fft<M, BIG>(v, fib, q, tw, -1);
+        fast::fft<M, CFG>(v, fib, q, tw, -1);
       }
     }
     if (KIND != K_SYNTH) {
-      fast::store_natural<M, BIG>(v, fib, q);
+      fast::store_natural<M, CFG>(v, fib, q);
       __syncthreads();
       if (valid) {
         const int qm = -q + ((-q) >> 3);
@@ -280,7 +301,7 @@ __global__ void __launch_bounds__(Geom<M, BIG>::T, Geom<M, BIG>::MINB) fast_pass
             xa = c0 * z0.x; ya = c0 * z0.y;
             xb = c0 * zh.x; yb = c0 * zh.y;
           } else {
-            const double2 a = fib[fast::lo_idx<M, BIG>(q, r)], b = fib[fast::hi_idx<M, BIG>(q, qm, r)];
+            const double2 a = fib[fast::lo_idx<M, CFG>(q, r)], b = fib[fast::hi_idx<M, CFG>(q, qm, r)];
             xa = c1 * (a.x + b.x);
             xb = c1 * (a.y - b.y);
             ya = c1 * (a.y + b.y);
@@ -318,42 +339,72 @@ struct Entry {
   int threads = 0, smem = 0, w = 0;
 };
 
-template <int M, bool S>
-Entry make(int kind, bool epi) {
+template <int M, bool S, int CFG>
+Entry make_cfg(int kind, bool epi) {
   Entry e;
-  // plain strided passes: big CTAs; gram / epilogue passes: pipelined small CTAs
-  constexpr bool BIG_OK = M <= 512;
-  const bool big = BIG_OK && S && !epi && (kind == K_SYNTH || kind == K_ANALYZE);
-  if (big) {
-    if constexpr (BIG_OK && S) {
-      using G = Geom<M, true>;
-      e.fn = kind == K_SYNTH ? fast_pass<M, true, K_SYNTH, false, true>
-                             : fast_pass<M, true, K_ANALYZE, false, true>;
-      e.threads = G::T;
-      e.smem = G::SMEM;
-      e.w = G::W;
-    }
-    return e;
-  }
-  using G = Geom<M, false>;
+  using G = Geom<M, CFG>;
   switch (kind) {
-    case K_SYNTH: e.fn = fast_pass<M, S, K_SYNTH, false, false>; break;
+    case K_SYNTH: e.fn = fast_pass<M, S, K_SYNTH, false, CFG>; break;
     case K_ANALYZE:
-      e.fn = epi ? fast_pass<M, S, K_ANALYZE, true, false> : fast_pass<M, S, K_ANALYZE, false, false>;
+      e.fn = epi ? fast_pass<M, S, K_ANALYZE, true, CFG> : fast_pass<M, S, K_ANALYZE, false, CFG>;
       break;
     case K_GRAM:
       if constexpr (!S)
-        e.fn = epi ? fast_pass<M, false, K_GRAM, true, false> : fast_pass<M, false, K_GRAM, false, false>;
+        e.fn = epi ? fast_pass<M, false, K_GRAM, true, CFG> : fast_pass<M, false, K_GRAM, false, CFG>;
       break;
     default:
       if constexpr (!S)
-        e.fn = epi ? fast_pass<M, false, K_RESID, true, false> : fast_pass<M, false, K_RESID, false, false>;
+        e.fn = epi ? fast_pass<M, false, K_RESID, true, CFG> : fast_pass<M, false, K_RESID, false, CFG>;
       break;
   }
   e.threads = G::T;
   e.smem = G::SMEM;
   e.w = G::W;
   return e;
+}
+
+// Default variant: plain strided passes on 512-thread CTAs without staging
+// (2 CTAs/SM at 64 registers); the fused gram pass and anything with an
+// epilogue on 256-thread CTAs with double-buffered cp.async staging.
+constexpr int kCfgLight = cfg_code(1, 0, 2);
+constexpr int kCfgHeavy = cfg_code(0, 2, 2);
+
+// Experiment hook (M = 512 only): FL_CFG_STRIDED / FL_CFG_CONTIG pick one of
+// the instantiated variants below for every plain-strided / other pass.
+template <bool S>
+Entry make512(int kind, bool epi, int cfg) {
+  switch (cfg) {
+    case cfg_code(1, 0, 2): return make_cfg<512, S, cfg_code(1, 0, 2)>(kind, epi);
+    case cfg_code(0, 1, 3): return make_cfg<512, S, cfg_code(0, 1, 3)>(kind, epi);
+    case cfg_code(0, 2, 2): return make_cfg<512, S, cfg_code(0, 2, 2)>(kind, epi);
+    case cfg_code(1, 1, 1): return make_cfg<512, S, cfg_code(1, 1, 1)>(kind, epi);
+    case cfg_code(1, 2, 1): return make_cfg<512, S, cfg_code(1, 2, 1)>(kind, epi);
+    case cfg_code(0, 0, 3): return make_cfg<512, S, cfg_code(0, 0, 3)>(kind, epi);
+    case cfg_code(0, 1, 2): return make_cfg<512, S, cfg_code(0, 1, 2)>(kind, epi);
+    default: return Entry();
+  }
+}
+
+int env_cfg(const char* name) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : -1;
+}
+
+template <int M, bool S>
+Entry make(int kind, bool epi) {
+  const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE);
+  if constexpr (M == 512) {
+    const int over_s = env_cfg("FL_CFG_STRIDED"), over_c = env_cfg("FL_CFG_CONTIG");
+    const int over = light ? over_s : over_c;
+    if (over >= 0) {
+      Entry e = make512<S>(kind, epi, over);
+      if (e.fn) return e;
+    }
+  }
+  if constexpr (M <= 512) {
+    if (light) return make_cfg<M, S, kCfgLight>(kind, epi);
+  }
+  return make_cfg<M, S, kCfgHeavy>(kind, epi);
 }
 
 template <bool S>
@@ -397,14 +448,22 @@ bool fast_supported(int m) { return m >= 16 && m <= 8192 && (m & (m - 1)) == 0; 
 
 int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int* nblocks,
                 cudaStream_t s) {
-  // per (m, layout, kind, epi) cache of the persistent grid size
-  static int cache[14][2][4][2] = {};
-  int lg = 0;
-  while ((1 << lg) < m) ++lg;
+  // persistent grid size per kernel variant (resident CTAs x SMs)
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> grids;
   Entry e = strided ? lookup<true>(m, kind, epi) : lookup<false>(m, kind, epi);
   if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");
-  int& grid_cap = cache[lg][strided][kind][epi];
-  if (!grid_cap) FL_TRY(grid_of(e, &grid_cap));
+  int grid_cap = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = grids.find((const void*)e.fn);
+    if (it == grids.end()) {
+      FL_TRY(grid_of(e, &grid_cap));
+      grids[(const void*)e.fn] = grid_cap;
+    } else {
+      grid_cap = it->second;
+    }
+  }
   const int64_t tiles = (A.G + e.w - 1) / e.w;
   const int grid = (int)std::min<int64_t>(tiles, grid_cap);
   e.fn<<<grid, e.threads, e.smem, s>>>(A);

@@ -14,9 +14,9 @@ for line in out.splitlines():
     m = re.search(r"Compiling entry function '(\S+)'", line)
     if m:
         cur = m.group(1)
-        d = re.search(r"fast_passILi(\d+)ELb(\d)ELi(\d)ELb(\d)E", cur)
+        d = re.search(r"fast_passILi(\d+)ELb(\d)ELi(\d)ELb(\d)ELi(\d+)E", cur)
         if d:
-            cur = f"fast_pass<M={d.group(1)},strided={d.group(2)},kind={d.group(3)},epi={d.group(4)}>"
+            cur = f"fast_pass<M={d.group(1)},s={d.group(2)},kind={d.group(3)},epi={d.group(4)},cfg={d.group(5)}>"
         else:
             cur = re.sub(r"_ZN2fl\d+_GLOBAL__N__\w+?_\d+(\w+?)E.*", r"\1", cur)[:60]
         continue
