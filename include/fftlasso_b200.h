@@ -102,6 +102,12 @@ FL_API int fl_synthesize(fl_plan_t plan, const double* beta, double* x, fl_strea
 /* analyze (fourier.py:225-235): beta = A^T x.  ``x`` may equal ``beta``. */
 FL_API int fl_analyze(fl_plan_t plan, const double* x, double* beta, fl_stream_t stream);
 
+/* One per-axis pass: _synthesize_axis (fourier.py:172-183, analysis = 0)
+ * or _analyze_axis (fourier.py:186-198, analysis = 1) along ``axis``.
+ * Building block of the slab-sharded transform; in may equal out. */
+FL_API int fl_axis_pass(fl_plan_t plan, int axis, int analysis, const double* in, double* out,
+                        fl_stream_t stream);
+
 /* ---- observation operators (masking.py) ------------------------------ */
 /* Mask bookkeeping: bits + per-word observed offsets from a byte mask
  * (masking.py:61-69 from_bool).  ``flags`` is a device uint8 array (1 =

@@ -55,6 +55,7 @@ SIGNATURES = {
     "fl_plan_n": (_I64, [_P]),
     "fl_synthesize": (_I, [_P, _P, _P, _P]),
     "fl_analyze": (_I, [_P, _P, _P, _P]),
+    "fl_axis_pass": (_I, [_P, _I, _I, _P, _P, _P]),
     "fl_mask_build": (_I, [_I64, _P, _P, _P, ctypes.POINTER(_I64), _P]),
     "fl_embed": (_I, [_I64, _P, _P, _P, _P, _P]),
     "fl_gather_observed": (_I, [_I64, _P, _P, _P, _P, _P]),

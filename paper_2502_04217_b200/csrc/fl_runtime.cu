@@ -210,6 +210,13 @@ int fl_analyze(fl_plan_t p, const double* x, double* beta, fl_stream_t stream) {
   return op_analyze(p, x, beta, (cudaStream_t)stream);
 }
 
+int fl_axis_pass(fl_plan_t p, int axis, int analysis, const double* in, double* out, fl_stream_t stream) {
+  if (!p || !in || !out) return fail(FL_E_VALUE, "null argument");
+  if (axis < 0 || axis >= p->ndim) return fail(FL_E_VALUE, "axis out of range");
+  return run_pass(p, axis, analysis ? K_ANALYZE : K_SYNTH, in, out, nullptr, nullptr, nullptr, nullptr,
+                  (cudaStream_t)stream);
+}
+
 int fl_gram(fl_plan_t p, const uint32_t* bits, const double* beta, double* out, fl_stream_t stream) {
   if (!p || !bits || !beta || !out) return fail(FL_E_VALUE, "null argument");
   return op_gram(p, bits, nullptr, false, beta, out, nullptr, nullptr, (cudaStream_t)stream);
