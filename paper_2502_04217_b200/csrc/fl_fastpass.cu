@@ -124,7 +124,7 @@ template <int M, bool STRIDED, int KIND, bool EPI, int CFG>
 __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(const PassArgs A) {
   using G = Geom<M, CFG>;
   constexpr int E = G::E, P = G::P, W = G::W, H = M / 2;
-  constexpr bool PIPE = G::PIPE;
+  constexpr int PIPE = G::PIPE;  // 0 none, 1 single, 2 double buffered staging
   extern __shared__ double2 smem[];
   __shared__ double red[32];
   int c, q;
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
   const double c0 = A.c0, c1 = A.c1;
   double acc = 0.0;
   const int64_t ntiles = (A.G + W - 1) / W;
-  if (PIPE) {
+  if (PIPE > 0) {
     if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, CFG>(A, blockIdx.x, stage0, c, q);
     cp_commit();
   }
@@ -158,9 +158,9 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
     }
     double2 v[E];
     if (KIND == K_ANALYZE) {
-      if (PIPE) {
+      if (PIPE > 0) {
 #pragma unroll
-        for (int r = 0; r < E; ++r) v[r] = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, q + r * P, c);
+        for (int r = 0; r < E; ++r) v[r] = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, q + r * P, c);
         refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
       } else {
         // base pointer of row q, rows advance by P*st (no per-element 64-bit multiplies)
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
       }
       fast::fft<M, CFG>(v, fib, q, tw, -1);
     } else {
-      if constexpr (PIPE) {
+      if constexpr (PIPE > 0) {
         // unpack straight from the staged raw rows into the natural layout:
         // Zin_k needs rows (k+1, k+h) for k < h and rows (M-k+1, M-k+h) above h
 #pragma unroll
@@ -191,21 +191,21 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
           double2 z;
           if (r < E / 2) {
             if (r == 0 && q == 0) {
-              const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, 0, c);
+              const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, 0, c);
               z = make_double2(c0 * a.x, c0 * a.y);
             } else {
-              const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, k + 1, c);
-              const double2 b = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, k + H, c);
+              const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, k + 1, c);
+              const double2 b = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, k + H, c);
               z = make_double2(c1 * (a.x - b.y), c1 * (b.x + a.y));
             }
           } else {
             if (r == E / 2 && q == 0) {
-              const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, 1, c);
+              const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, 1, c);
               z = make_double2(c0 * a.x, c0 * a.y);
             } else {
               const int j = M - k;
-              const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, j + 1, c);
-              const double2 b = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, j + H, c);
+              const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, j + 1, c);
+              const double2 b = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, j + H, c);
               z = make_double2(c1 * (a.x + b.y), c1 * (a.y - b.x));
             }
           }
@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
         for (int r = 0; r < E / 2; ++r) {
           const int j = q + r * P;
           const bool j0 = r == 0 && q == 0;
-          const double2 a = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, j0 ? 0 : j + 1, c);
-          const double2 b = raw<M, STRIDED, PIPE, CFG>(A, st, Q, valid, j0 ? 1 : j + H, c);
+          const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, j0 ? 0 : j + 1, c);
+          const double2 b = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, j0 ? 1 : j + H, c);
           const double xa = a.x, ya = a.y, xb = b.x, yb = b.y;
           if (j0) {
             fib[0] = make_double2(c0 * xa, c0 * ya);
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
     }
     __syncthreads();
   }
-  if (PIPE) cp_wait<0>();
+  if (PIPE > 0) cp_wait<0>();
   if (EPI && A.epi.partials) {
     const double s = block_reduce(acc, SumOp(), red);
     if (threadIdx.x == 0) A.epi.partials[blockIdx.x] = s;
