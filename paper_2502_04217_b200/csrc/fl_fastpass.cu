@@ -365,9 +365,10 @@ Entry make_cfg(int kind, bool epi) {
 
 // Default variant: plain strided passes on 512-thread CTAs without staging
 // (2 CTAs/SM at 64 registers); the fused gram pass and anything with an
-// epilogue on 256-thread CTAs with double-buffered cp.async staging.
+// epilogue on 256-thread CTAs with single-buffer cp.async staging (tools/
+// sweep_cfg.py on B200: 0.80 ms vs 0.92 double-buffered for the 512^3 gram pass).
 constexpr int kCfgLight = cfg_code(1, 0, 2);
-constexpr int kCfgHeavy = cfg_code(0, 2, 2);
+constexpr int kCfgHeavy = cfg_code(0, 1, 2);
 
 // Experiment hook (M = 512 only): FL_CFG_STRIDED / FL_CFG_CONTIG pick one of
 // the instantiated variants below for every plain-strided / other pass.

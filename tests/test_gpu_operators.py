@@ -159,3 +159,29 @@ def test_interior_violation_raises():
     bad[3] = np.nan
     with pytest.raises(fl.InteriorViolationError):
         ns.barrier_diagonals(s, s, bad, s)
+
+
+@pytest.mark.parametrize("dims", [(256, 256, 256), (2048, 2048), (512, 64, 64), (8192, 256)])
+def test_large_grid_matches_oracle(dims):
+    """Full-size grids (hundreds of tiles per persistent CTA) against the oracle.
+
+    Round trips and golden vectors at small n cannot see a tile-mapping error
+    that keeps the operator orthogonal; direct comparison at scale does.
+    """
+    from paper_2502_04217_b200 import workloads
+
+    rng = np.random.default_rng(sum(dims))
+    shape = fl.GridShape(dims)
+    if len(dims) == 3 and len(set(dims)) == 1:
+        flags = workloads.bragg_flags(dims[0])
+    else:
+        flags = rng.random(shape.n) < 0.15
+    mask = fl.Mask.from_bool(flags, shape)
+    om = orc.make_mask(dims, flags=flags)
+    beta = rng.standard_normal(shape.n)
+    tol = 1e-12 * np.abs(beta).max()
+    assert np.max(np.abs(fl.synthesize(beta, shape) - orc.synthesize(beta, dims))) <= tol
+    assert np.max(np.abs(fl.analyze(beta, shape) - orc.analyze(beta, dims))) <= tol
+    assert np.max(np.abs(fl.gram(beta, mask) - orc.gram(beta, om))) <= tol
+    w = rng.standard_normal(mask.n_observed)
+    assert np.max(np.abs(fl.observe_adjoint(w, mask) - orc.observe_adjoint(w, om))) <= 1e-12 * np.abs(w).max()
