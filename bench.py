@@ -221,9 +221,16 @@ def run_b200(args, rank: int, world: int):
     dom = int(np.argmax(pass_ms))
     op_bytes = sum(alg)
     op_gbps = op_bytes / (ms_per_step * 1e6)
+    traffic = None
+    try:  # ncu dram bytes per launch of the same kernel, committed under profiles/
+        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as fh:
+            if side == 512:
+                traffic = json.load(fh)["kernels"].get(PASS_NAMES_3D[dom])
+    except Exception:
+        traffic = None
     roofline = {"bound": "hbm", "kernel": PASS_NAMES_3D[dom], "achieved": round(alg[dom] / pass_ms[dom] / 1e6, 1),
                 "peak": peak, "unit": "GB/s", "frac": round(alg[dom] / pass_ms[dom] / 1e6 / peak, 4),
-                "traffic": None, "peak_source": peak_src,
+                "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_launch": alg[dom]}
     model_bytes = 120.125 * n  # SURVEY 8d operator model (epilogue fused)
     op_gbps = model_bytes / (ms_per_step * 1e6)
