@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
   double2* stage1 = stage0 + W * M;
   const double2* tw = A.plan.tw;
   const double c0 = A.c0, c1 = A.c1;
-  double acc = 0.0;
+  double acc = 0.0, nrm = 0.0;
   const int64_t ntiles = (A.G + W - 1) / W;
   if (PIPE > 0) {
     if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, CFG>(A, blockIdx.x, stage0, c, q);
@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
             } else {
               z.y = 0.0;
             }
+            if (KIND == K_GRAM) nrm += z.x * z.x + z.y * z.y;  // ||Z A beta||^2 = beta . G beta
           }
           v[r] = z;
         }
@@ -331,6 +332,10 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
   if (EPI && A.epi.partials) {
     const double s = block_reduce(acc, SumOp(), red);
     if (threadIdx.x == 0) A.epi.partials[blockIdx.x] = s;
+  }
+  if (KIND == K_GRAM && A.nrm_partials) {
+    const double s = block_reduce(nrm, SumOp(), red);
+    if (threadIdx.x == 0) A.nrm_partials[blockIdx.x] = s;
   }
 }
 

@@ -45,6 +45,12 @@ int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out
              const uint32_t* bits, const double* bhat, const KktEpi* epi, int* nblocks,
              cudaStream_t s);
 
+int run_pass_n(const fl_plan* p, int axis, int kind, const double* in, double* out,
+               const uint32_t* bits, const double* bhat, const KktEpi* epi, int* nblocks,
+               double* nrm_partials, cudaStream_t s);
+int op_gram_norm(const fl_plan* p, const uint32_t* bits, const double* in, double* out,
+                 double* nrm_partials, int* nblocks, bool* have_norm, cudaStream_t s);
+
 struct PassArgs;
 int long_factor(int m, int* m1, int* m2);
 int run_long(const fl_plan* p, int axis, int kind, const PassArgs& A, bool strided, const KktEpi* epi,
@@ -69,5 +75,14 @@ int pcg_update(int64_t n, const double* sig1, const double* sig2, const double* 
                const double* kp_bot, double* partials, int* nblocks, cudaStream_t s);
 int pcg_pupdate(int64_t n, const double* sig1, const double* sig2, const double* r, double beta,
                 double* p, cudaStream_t s);
+// restructured PCG: curvature = ||Z A p_beta||^2 (fused gram pass) + diagonal form
+int pcg2_init(int64_t n, const double* sig1, const double* sig2, const double* rhs, double* x, double* r,
+              double* p, double* partials, int* nblocks, cudaStream_t s);
+int pcg2_update(int64_t n, const double* sig1, const double* sig2, const double* rho, const double* curv_g,
+                const double* curv_d, double* x, double* r, const double* p, const double* gp,
+                double* partials, int* nblocks, cudaStream_t s);
+int pcg2_pupdate(int64_t n, const double* sig1, const double* sig2, const double* r, double beta, double* p,
+                 double* partials, int* nblocks, cudaStream_t s);
+int dot_partials(int64_t n, const double* a, const double* b, double* partials, int* nblocks, cudaStream_t s);
 
 }  // namespace fl

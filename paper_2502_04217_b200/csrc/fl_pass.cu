@@ -100,7 +100,7 @@ __device__ void load_plain(const PassArgs& A, double2* buf, int64_t g0, int nf) 
 
 // ---- middle stage of the fused last-axis pass: Z (b_hat - x) or Z x ----
 template <bool RESID>
-__device__ void apply_mask(const PassArgs& A, double2* buf, int64_t g0, int nf) {
+__device__ void apply_mask(const PassArgs& A, double2* buf, int64_t g0, int nf, double& nrm) {
   const int F = A.F, m = A.m;
   for (int idx = threadIdx.x; idx < F * m; idx += blockDim.x) {
     int f, k;
@@ -118,6 +118,7 @@ __device__ void apply_mask(const PassArgs& A, double2* buf, int64_t g0, int nf) 
     } else {
       z.y = 0.0;
     }
+    if (!RESID) nrm += z.x * z.x + z.y * z.y;
     buf[f * A.fs + k] = z;
   }
 }
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) axis_pass(const PassArgs A) {
   __shared__ double red[32];
   double2* b0 = smem;
   double2* b1 = smem + A.F * A.fs;
-  double acc = 0.0;
+  double acc = 0.0, nrm = 0.0;
   for (int64_t tile = blockIdx.x; tile * A.F < A.G; tile += gridDim.x) {
     const int64_t g0 = tile * A.F;
     const int64_t rem = A.G - g0;
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(kThreads) axis_pass(const PassArgs A) {
       __syncthreads();
       res = fft_tile(b0, b1, A.F, A.fs, A.plan, +1);
       if (KIND == K_GRAM || KIND == K_RESID) {
-        apply_mask<KIND == K_RESID>(A, res, g0, nf);
+        apply_mask<KIND == K_RESID>(A, res, g0, nf, nrm);
         __syncthreads();
         res = fft_tile(res, res == b0 ? b1 : b0, A.F, A.fs, A.plan, -1);
       }
@@ -209,6 +210,10 @@ __global__ void __launch_bounds__(kThreads) axis_pass(const PassArgs A) {
   if (EPI && A.epi.partials) {
     const double s = block_reduce(acc, SumOp(), red);
     if (threadIdx.x == 0) A.epi.partials[blockIdx.x] = s;
+  }
+  if (KIND == K_GRAM && A.nrm_partials) {
+    const double s = block_reduce(nrm, SumOp(), red);
+    if (threadIdx.x == 0) A.nrm_partials[blockIdx.x] = s;
   }
 }
 
@@ -236,6 +241,12 @@ int set_smem_attr(KernelFn k) {
 int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out,
              const uint32_t* bits, const double* bhat, const KktEpi* epi, int* nblocks,
              cudaStream_t s) {
+  return run_pass_n(p, axis, kind, in, out, bits, bhat, epi, nblocks, nullptr, s);
+}
+
+int run_pass_n(const fl_plan* p, int axis, int kind, const double* in, double* out,
+               const uint32_t* bits, const double* bhat, const KktEpi* epi, int* nblocks,
+               double* nrm_partials, cudaStream_t s) {
   static bool attrs_set[2][4][2] = {};
   const bool strided = axis < p->ndim - 1;
   if ((kind == K_GRAM || kind == K_RESID) && strided)
@@ -262,6 +273,7 @@ int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out
   A.plan = p->axis[axis];
   A.bits = bits;
   A.bhat = bhat;
+  A.nrm_partials = nrm_partials;
   if (epi) A.epi = *epi;
   if (p->lng[axis].on) return run_long(p, axis, kind, A, strided, epi, nblocks, s);
   static const bool force_generic = [] {
@@ -342,6 +354,26 @@ int op_gram(const fl_plan* p, const uint32_t* bits, const double* bhat, bool res
   for (int a = d - 2; a >= 0; --a)
     FL_TRY(run_pass(p, a, K_ANALYZE, out, out, nullptr, nullptr, a == 0 ? epi : nullptr,
                     a == 0 ? nblocks : nullptr, s));
+  return FL_OK;
+}
+
+// g = G beta with the fused-pass partials of ||Z A beta||^2 = beta . G beta
+// (the matrix part of the PCG curvature).  Returns FL_E_VALUE via *have_norm
+// = false when the mask pass cannot produce them (four-step long axis).
+int op_gram_norm(const fl_plan* p, const uint32_t* bits, const double* in, double* out,
+                 double* nrm_partials, int* nblocks, bool* have_norm, cudaStream_t s) {
+  const int d = p->ndim;
+  *have_norm = !p->lng[d - 1].on;
+  double* np = *have_norm ? nrm_partials : nullptr;
+  if (d == 1) return run_pass_n(p, 0, K_GRAM, in, out, bits, nullptr, nullptr, nblocks, np, s);
+  const double* src = in;
+  for (int a = 0; a < d - 1; ++a) {
+    FL_TRY(run_pass(p, a, K_SYNTH, src, out, nullptr, nullptr, nullptr, nullptr, s));
+    src = out;
+  }
+  FL_TRY(run_pass_n(p, d - 1, K_GRAM, src, out, bits, nullptr, nullptr, nblocks, np, s));
+  for (int a = d - 2; a >= 0; --a)
+    FL_TRY(run_pass(p, a, K_ANALYZE, out, out, nullptr, nullptr, nullptr, nullptr, s));
   return FL_OK;
 }
 

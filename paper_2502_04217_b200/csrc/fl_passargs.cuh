@@ -20,6 +20,7 @@ struct PassArgs {
   const uint32_t* bits;
   const double* bhat;
   KktEpi epi;
+  double* nrm_partials;  // K_GRAM: per-block ||Z A beta||^2 partials (nullable)
 };
 
 // Geometry of fibre pair g: element k of fibre x at bx + k*st, of y at by + k*st.

@@ -491,6 +491,80 @@ __global__ void k_kkt_epilogue(int64_t n2, double2* __restrict__ g, const double
   if (partials) emit(acc, SumOp(), red, partials, 0);
 }
 
+// ---- restructured PCG (g = G p_beta instead of materialised K p) ----
+// d.(K - G)d = pb (L1 pb + L2 pz) + pz (L2 pb + L1 pz): the diagonal part of
+// the curvature, accumulated where p is written (init / p-update).
+__device__ __forceinline__ double diag_quad(double l1, double l2, double pb, double pz) {
+  return pb * (l1 * pb + l2 * pz) + pz * (l2 * pb + l1 * pz);
+}
+
+__global__ void k_pcg2_init(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
+                            const double* __restrict__ rhs, double* __restrict__ x,
+                            double* __restrict__ r, double* __restrict__ p, double* __restrict__ partials) {
+  __shared__ double red[32];
+  double rho = 0.0, dq = 0.0;
+  GRID_LOOP(i, n) {
+    const double rb = rhs[i], rc = rhs[n + i];
+    const Pinv P(g1[i], g2[i]);
+    const double zt = P.top(rb, rc), zb = P.bot(rb, rc);
+    x[i] = 0.0;
+    x[n + i] = 0.0;
+    r[i] = rb;
+    r[n + i] = rc;
+    p[i] = zt;
+    p[n + i] = zb;
+    rho += mul(rb, zt) + mul(rc, zb);
+    dq += diag_quad(P.l1, P.l2, zt, zb);
+  }
+  emit(rho, SumOp(), red, partials, 0);
+  emit(dq, SumOp(), red, partials, 1);
+}
+
+// x += alpha p; r -= alpha K p with K p formed in registers from g = G p_beta
+// exactly as apply_kkt (newton_system.py:150-151); z = P^{-1} r; rho partials.
+__global__ void k_pcg2_update(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
+                              const double* __restrict__ rho_p, const double* __restrict__ curv_g,
+                              const double* __restrict__ curv_d, double* __restrict__ x,
+                              double* __restrict__ r, const double* __restrict__ p,
+                              const double* __restrict__ gp, double* __restrict__ partials) {
+  __shared__ double red[32];
+  const double alpha = dvd(*rho_p, add(*curv_g, *curv_d));
+  double rho = 0.0;
+  GRID_LOOP(i, n) {
+    const double pt = p[i], pb = p[n + i];
+    const double a1 = g1[i], a2 = g2[i];
+    const double l1 = add(a1, a2), l2 = sub(a1, a2);
+    const double kt = add(add(gp[i], mul(l1, pt)), mul(l2, pb));
+    const double kb = add(mul(l2, pt), mul(l1, pb));
+    x[i] = add(x[i], mul(alpha, pt));
+    x[n + i] = add(x[n + i], mul(alpha, pb));
+    const double rt = sub(r[i], mul(alpha, kt));
+    const double rb = sub(r[n + i], mul(alpha, kb));
+    r[i] = rt;
+    r[n + i] = rb;
+    const Pinv P(a1, a2);
+    rho += mul(rt, P.top(rt, rb)) + mul(rb, P.bot(rt, rb));
+  }
+  emit(rho, SumOp(), red, partials, 0);
+}
+
+__global__ void k_pcg2_pupdate(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
+                               const double* __restrict__ r, double beta, double* __restrict__ p,
+                               double* __restrict__ partials) {
+  __shared__ double red[32];
+  double dq = 0.0;
+  GRID_LOOP(i, n) {
+    const double rt = r[i], rb = r[n + i];
+    const Pinv P(g1[i], g2[i]);
+    const double pt = add(P.top(rt, rb), mul(beta, p[i]));
+    const double pb = add(P.bot(rt, rb), mul(beta, p[n + i]));
+    p[i] = pt;
+    p[n + i] = pb;
+    dq += diag_quad(P.l1, P.l2, pt, pb);
+  }
+  emit(dq, SumOp(), red, partials, 0);
+}
+
 // Reduce ``nk`` partial rows and fetch them to the host.
 int reduce_fetch(Scratch* sc, int grid, int nk, const int* kinds, double* out, cudaStream_t s) {
   FL_TRY(finish_reduce(sc->partials, grid, nk, kinds, sc->result, s));
@@ -531,6 +605,42 @@ int kkt_epilogue(int64_t n, double* g, const double* pb, const double* pz, const
                                     partials);
   FL_LAUNCH_CHECK();
   if (nblocks) *nblocks = grid;
+  return FL_OK;
+}
+
+int pcg2_init(int64_t n, const double* sig1, const double* sig2, const double* rhs, double* x, double* r,
+              double* p, double* partials, int* nblocks, cudaStream_t s) {
+  const int grid = grid_for(n, T);
+  k_pcg2_init<<<grid, T, 0, s>>>(n, sig1, sig2, rhs, x, r, p, partials);
+  FL_LAUNCH_CHECK();
+  *nblocks = grid;
+  return FL_OK;
+}
+
+int pcg2_update(int64_t n, const double* sig1, const double* sig2, const double* rho, const double* curv_g,
+                const double* curv_d, double* x, double* r, const double* p, const double* gp,
+                double* partials, int* nblocks, cudaStream_t s) {
+  const int grid = grid_for(n, T);
+  k_pcg2_update<<<grid, T, 0, s>>>(n, sig1, sig2, rho, curv_g, curv_d, x, r, p, gp, partials);
+  FL_LAUNCH_CHECK();
+  *nblocks = grid;
+  return FL_OK;
+}
+
+int pcg2_pupdate(int64_t n, const double* sig1, const double* sig2, const double* r, double beta, double* p,
+                 double* partials, int* nblocks, cudaStream_t s) {
+  const int grid = grid_for(n, T);
+  k_pcg2_pupdate<<<grid, T, 0, s>>>(n, sig1, sig2, r, beta, p, partials);
+  FL_LAUNCH_CHECK();
+  *nblocks = grid;
+  return FL_OK;
+}
+
+int dot_partials(int64_t n, const double* a, const double* b, double* partials, int* nblocks, cudaStream_t s) {
+  const int grid = grid_for(n, T);
+  k_dot<<<grid, T, 0, s>>>(n, a, b, partials);
+  FL_LAUNCH_CHECK();
+  *nblocks = grid;
   return FL_OK;
 }
 

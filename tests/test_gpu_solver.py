@@ -218,3 +218,38 @@ def test_ipm_step_and_check_convergence_match_oracle(rng):
     for f in ("stationarity", "dual_equality", "multiplier_gap", "primal", "complementarity"):
         assert getattr(c, f) == pytest.approx(oc[f], rel=1e-7)
     assert c.centrality_ok == oc["centrality_ok"]
+
+
+def test_pcg_v1_matches_v2():
+    """The materialised-Kp PCG (FL_PCG_V1=1) and the default fused-curvature PCG agree."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    code = r'''
+import sys, json, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_2502_04217_b200 as fl
+from conftest import load_golden
+out = {}
+for name in ("c1_4096", "c3_32", "harm_16"):
+    g = load_golden("solve_" + name)
+    dims = tuple(int(d) for d in g["dims"])
+    beta, rep = fl.solve(g["b"], fl.Mask(g["missing"], fl.GridShape(dims)), fl.IpmConfig(lam=float(g["lam"])))
+    out[name] = [rep.krylov_counts, rep.final_objective, beta.tolist()[:64]]
+print(json.dumps(out))
+''' % (REPO, REPO + "/tests")
+    res = {}
+    for v1 in ("0", "1"):
+        env = dict(os.environ, FL_PCG_V1=v1)
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[v1] = json.loads(out.stdout.strip().splitlines()[-1])
+    for name in res["0"]:
+        k0, o0, b0 = res["0"][name]
+        k1, o1, b1 = res["1"][name]
+        assert all(abs(a - b) <= 1 for a, b in zip(k0, k1))
+        assert abs(o0 - o1) <= 1e-9 * abs(o1)
+        assert np.allclose(b0, b1, atol=1e-7)
