@@ -96,6 +96,12 @@ FL_API int fl_plan_create(int ndim, const int64_t* dims, int device, fl_plan_t* 
 FL_API int fl_plan_destroy(fl_plan_t plan);
 FL_API int64_t fl_plan_n(fl_plan_t plan);
 
+/* Local plan of a slab-sharded grid: only the axes set in ``transform_axes``
+ * (bit a = axis a) are planned/validated (even, >= 2); the others are batch
+ * extents of any size >= 1 (slab heights d0/P, d1/P). */
+FL_API int fl_plan_create_ex(int ndim, const int64_t* dims, int transform_axes, int device,
+                             fl_plan_t* out);
+
 /* ---- transforms (fourier.py) ----------------------------------------- */
 /* synthesize (fourier.py:201-222): x = A beta.  ``beta`` may equal ``x``. */
 FL_API int fl_synthesize(fl_plan_t plan, const double* beta, double* x, fl_stream_t stream);
@@ -109,6 +115,29 @@ FL_API int fl_axis_pass(fl_plan_t plan, int axis, int analysis, const double* in
                         fl_stream_t stream);
 
 /* ---- observation operators (masking.py) ------------------------------ */
+/* The fused last-axis pass on its own: synthesis along the last (contiguous)
+ * axis, Z x (b_hat == NULL: gram, masking.py:116-117) or Z (b_hat - x)
+ * (residual), analysis along the same axis.  With ``nrm_host`` != NULL and
+ * b_hat == NULL also returns ||Z x||^2 (synchronises).  This is the middle
+ * step of the slab-sharded gram, run in the Y-slab layout. */
+FL_API int fl_fused_mask_pass(fl_plan_t plan, const uint32_t* miss_bits, const double* b_hat,
+                              const double* in, double* out, double* nrm_host, fl_stream_t stream);
+/* Slab transposes of a (d0, d1, d2) grid over P ranks (d0 = P*a, d1 = P*b):
+ *   X-slab of rank r: rows i0 in [r a, (r+1) a), local layout (a, d1, d2);
+ *   Y-slab of rank r: i1 in [r b, (r+1) b), local layout (b, d2, d0) -- axis 0
+ *   made contiguous so the fused mask pass runs on it.
+ * pack_x:   X-slab -> send buffer of P blocks (a, b, d2), block s for rank s.
+ * unpack_y: receive buffer of P blocks (a, b, d2) (block r from rank r) -> Y-slab.
+ * pack_y / unpack_x: the inverse pair (Y-slab -> blocks -> X-slab). */
+FL_API int fl_slab_pack_x(int64_t a, int64_t d1, int64_t d2, int nranks, const double* x_slab,
+                          double* send, fl_stream_t stream);
+FL_API int fl_slab_unpack_y(int64_t a, int64_t b, int64_t d2, int nranks, const double* recv,
+                            double* y_slab, fl_stream_t stream);
+FL_API int fl_slab_pack_y(int64_t a, int64_t b, int64_t d2, int nranks, const double* y_slab,
+                          double* send, fl_stream_t stream);
+FL_API int fl_slab_unpack_x(int64_t a, int64_t d1, int64_t d2, int nranks, const double* recv,
+                            double* x_slab, fl_stream_t stream);
+
 /* Mask bookkeeping: bits + per-word observed offsets from a byte mask
  * (masking.py:61-69 from_bool).  ``flags`` is a device uint8 array (1 =
  * missing); writes n_words = ceil(n/32) words and offsets; returns the
@@ -182,6 +211,27 @@ FL_API int fl_pcg_kkt(fl_plan_t plan, const uint32_t* miss_bits, const double* s
                const double* sigma2, const double* rhs, double* x, double* work,
                double abs_tol, double rel_tol, int64_t max_iters, fl_pcg_result* res,
                double* history, int64_t max_history, fl_stream_t stream);
+
+/* Step-wise PCG kernels of fl_pcg_kkt (v2) for callers that combine the
+ * scalars across ranks themselves (slab-sharded solve).  All return LOCAL
+ * partial sums to the host (synchronise):
+ *   init:    x = 0, r = rhs, p = P^{-1} r;  out[0] = r.p, out[1] = p.(K-G)p
+ *   update:  with K p formed from g = G p_beta: x += alpha p, r -= alpha K p;
+ *            out[0] = r.P^{-1}r
+ *   pupdate: p = P^{-1} r + beta p;  out[0] = p.(K-G)p */
+FL_API int fl_pcg_step_init(int64_t n, const double* sigma1, const double* sigma2, const double* rhs,
+                            double* x, double* r, double* p, double* out, fl_stream_t stream);
+FL_API int fl_pcg_step_update(int64_t n, const double* sigma1, const double* sigma2, double alpha,
+                              double* x, double* r, const double* p, const double* g, double* out,
+                              fl_stream_t stream);
+FL_API int fl_pcg_step_pupdate(int64_t n, const double* sigma1, const double* sigma2, const double* r,
+                               double beta, double* p, double* out, fl_stream_t stream);
+/* Objective pieces on a full (or slab) grid given x = A beta:
+ * out[0] = sum over observed (b_hat - x)^2, out[1] = sum |beta| (beta may be
+ * NULL -> 0).  ipm.py:209-211. */
+FL_API int fl_objective_terms(int64_t n, const uint32_t* miss_bits, const double* b_hat,
+                              const double* x, int64_t n_beta, const double* beta, double* out,
+                              fl_stream_t stream);
 
 /* ---- IPM outer step (ipm.py) ------------------------------------------ */
 /* initial_state (ipm.py:214-238): beta=0, z=s=1, y=nu=0.5*lam. */

@@ -51,11 +51,17 @@ SIGNATURES = {
     "fl_version": (_I, []),
     "fl_last_error": (ctypes.c_char_p, []),
     "fl_plan_create": (_I, [_I, ctypes.POINTER(_I64), _I, ctypes.POINTER(_P)]),
+    "fl_plan_create_ex": (_I, [_I, ctypes.POINTER(_I64), _I, _I, ctypes.POINTER(_P)]),
     "fl_plan_destroy": (_I, [_P]),
     "fl_plan_n": (_I64, [_P]),
     "fl_synthesize": (_I, [_P, _P, _P, _P]),
     "fl_analyze": (_I, [_P, _P, _P, _P]),
     "fl_axis_pass": (_I, [_P, _I, _I, _P, _P, _P]),
+    "fl_fused_mask_pass": (_I, [_P, _P, _P, _P, _P, ctypes.POINTER(_D), _P]),
+    "fl_slab_pack_x": (_I, [_I64, _I64, _I64, _I, _P, _P, _P]),
+    "fl_slab_unpack_x": (_I, [_I64, _I64, _I64, _I, _P, _P, _P]),
+    "fl_slab_pack_y": (_I, [_I64, _I64, _I64, _I, _P, _P, _P]),
+    "fl_slab_unpack_y": (_I, [_I64, _I64, _I64, _I, _P, _P, _P]),
     "fl_mask_build": (_I, [_I64, _P, _P, _P, ctypes.POINTER(_I64), _P]),
     "fl_embed": (_I, [_I64, _P, _P, _P, _P, _P]),
     "fl_gather_observed": (_I, [_I64, _P, _P, _P, _P, _P]),
@@ -69,6 +75,10 @@ SIGNATURES = {
     "fl_recover_eliminated": (_I, [_I64] + [_P] * 12 + [_P]),
     "fl_pcg_work_doubles": (_I64, [_I64]),
     "fl_pcg_kkt": (_I, [_P] * 7 + [_D, _D, _I64, ctypes.POINTER(FlPcgResult), _P, _I64, _P]),
+    "fl_pcg_step_init": (_I, [_I64] + [_P] * 6 + [ctypes.POINTER(_D), _P]),
+    "fl_pcg_step_update": (_I, [_I64, _P, _P, _D, _P, _P, _P, _P, ctypes.POINTER(_D), _P]),
+    "fl_pcg_step_pupdate": (_I, [_I64, _P, _P, _P, _D, _P, ctypes.POINTER(_D), _P]),
+    "fl_objective_terms": (_I, [_I64, _P, _P, _P, _I64, _P, ctypes.POINTER(_D), _P]),
     "fl_ipm_init": (_I, [_I64, ctypes.POINTER(FlState), _D, _P]),
     "fl_ipm_assess": (_I, [_I64, ctypes.POINTER(FlState), _P, _D, _D, ctypes.POINTER(FlAssess), _P]),
     "fl_ipm_ratios": (_I, [_I64, ctypes.POINTER(FlState), _P, _P, _D, _P, _P,

@@ -24,6 +24,7 @@ struct fl_plan {
   int device = 0;
   fl::AxisPlan axis[3];
   LongAxis lng[3];
+  bool planned[3] = {true, true, true};  // false: batch extent of a slab plan
   std::vector<void*> owned;  // device allocations (twiddle tables)
 };
 

@@ -249,6 +249,7 @@ int run_pass_n(const fl_plan* p, int axis, int kind, const double* in, double* o
                double* nrm_partials, cudaStream_t s) {
   static bool attrs_set[2][4][2] = {};
   const bool strided = axis < p->ndim - 1;
+  if (!p->planned[axis]) return fail(FL_E_VALUE, "axis " + std::to_string(axis) + " is a batch extent of this plan");
   if ((kind == K_GRAM || kind == K_RESID) && strided)
     return fail(FL_E_VALUE, "fused mask pass must run on the contiguous axis");
   PassArgs A;

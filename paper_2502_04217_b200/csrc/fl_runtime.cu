@@ -164,13 +164,19 @@ int fl_version(void) { return 1; }
 const char* fl_last_error(void) { return g_err.c_str(); }
 
 int fl_plan_create(int ndim, const int64_t* dims, int device, fl_plan_t* out) {
+  return fl_plan_create_ex(ndim, dims, (1 << ndim) - 1, device, out);
+}
+
+int fl_plan_create_ex(int ndim, const int64_t* dims, int transform_axes, int device, fl_plan_t* out) {
   if (!out) return fail(FL_E_VALUE, "null output");
   *out = nullptr;
   if (ndim < 1 || ndim > 3) return fail(FL_E_SHAPE, "need 1 to 3 axes, got " + std::to_string(ndim));
   int64_t n = 1;
   for (int a = 0; a < ndim; ++a) {
-    if (dims[a] < 2 || dims[a] % 2)
+    const bool tr = (transform_axes >> a) & 1;
+    if (tr && (dims[a] < 2 || dims[a] % 2))
       return fail(FL_E_SHAPE, "every axis must be even and >= 2, got " + std::to_string(dims[a]));
+    if (!tr && dims[a] < 1) return fail(FL_E_SHAPE, "batch extent must be >= 1");
     if (dims[a] > (1 << 30)) return fail(FL_E_SHAPE, "axis too long");
     n *= dims[a];
   }
@@ -181,6 +187,8 @@ int fl_plan_create(int ndim, const int64_t* dims, int device, fl_plan_t* out) {
   p->device = device;
   for (int a = 0; a < ndim; ++a) p->dims[a] = dims[a];
   for (int a = 0; a < ndim; ++a) {
+    p->planned[a] = (transform_axes >> a) & 1;
+    if (!p->planned[a]) continue;
     int st = build_axis(p, a);
     if (st != FL_OK) {
       fl_plan_destroy(p);
@@ -215,6 +223,27 @@ int fl_axis_pass(fl_plan_t p, int axis, int analysis, const double* in, double* 
   if (axis < 0 || axis >= p->ndim) return fail(FL_E_VALUE, "axis out of range");
   return run_pass(p, axis, analysis ? K_ANALYZE : K_SYNTH, in, out, nullptr, nullptr, nullptr, nullptr,
                   (cudaStream_t)stream);
+}
+
+int fl_fused_mask_pass(fl_plan_t p, const uint32_t* bits, const double* bhat, const double* in, double* out,
+                       double* nrm_host, fl_stream_t stream) {
+  if (!p || !bits || !in || !out) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int last = p->ndim - 1;
+  const bool want = nrm_host && !bhat;
+  if (want && p->lng[last].on) return fail(FL_E_VALUE, "norm output not available on four-step axes");
+  Scratch* sc = nullptr;
+  FL_TRY(scratch(&sc));
+  int nb = 0;
+  FL_TRY(run_pass_n(p, last, bhat ? K_RESID : K_GRAM, in, out, bits, bhat, nullptr, &nb,
+                    want ? sc->partials : nullptr, s));
+  if (want) {
+    const int kind = RED_SUM;
+    FL_TRY(finish_reduce(sc->partials, nb, 1, &kind, sc->result, s));
+    FL_TRY(fetch_results(sc, 1, s));
+    *nrm_host = sc->host[0];
+  }
+  return FL_OK;
 }
 
 int fl_gram(fl_plan_t p, const uint32_t* bits, const double* beta, double* out, fl_stream_t stream) {

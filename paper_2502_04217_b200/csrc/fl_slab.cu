@@ -1,0 +1,135 @@
+// Slab transposes for the sharded 3D transform (row e of SURVEY 8).
+//
+// Grid (d0, d1, d2), P ranks, d0 = P a, d1 = P b.  X-slab (a, d1, d2): axes 1
+// and 2 local.  Y-slab (b, d2, d0): axis 0 local AND contiguous, so the fused
+// synth / mask / analysis pass of fl_fastpass.cu runs on it unchanged.  The
+// all-to-all moves P blocks of (a, b, d2) per rank; these kernels build and
+// consume those blocks.  X-side kernels are contiguous runs of d2 (16-byte
+// moves); Y-side kernels transpose (i0, i2) through 32x33 shared tiles.
+#include <algorithm>
+
+#include "fl_common.cuh"
+#include "fl_internal.h"
+
+namespace fl {
+namespace {
+
+constexpr int T = 256;
+
+// send[s][i0][j1][i2] = x[i0][s b + j1][i2]   (PACK = true)
+// x[i0][s b + j1][i2] = recv[s][i0][j1][i2]   (PACK = false)
+template <bool PACK>
+__global__ void k_x_blocks(int64_t a, int64_t d1, int64_t d2h, int P, const double2* __restrict__ src,
+                           double2* __restrict__ dst) {
+  const int64_t b = d1 / P;
+  const int64_t total = a * d1 * d2h;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    // o indexes the block layout (s, i0, j1, i2h)
+    const int64_t i2 = o % d2h;
+    int64_t t = o / d2h;
+    const int64_t j1 = t % b;
+    t /= b;
+    const int64_t i0 = t % a;
+    const int64_t s = t / a;
+    const int64_t xi = (i0 * d1 + s * b + j1) * d2h + i2;
+    if (PACK) dst[o] = src[xi];
+    else dst[xi] = src[o];
+  }
+}
+
+// Y-slab <-> blocks: y[j1][i2][r a + i0] <-> blk[r][i0][j1][i2].
+// One CTA per (r, j1, 32x32 tile of (i0, i2)); smem tile padded to 33.
+template <bool TO_Y>
+__global__ void k_y_blocks(int64_t a, int64_t b, int64_t d2, int P, const double* __restrict__ src,
+                           double* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int64_t d0 = a * P;
+  const int64_t t0 = (a + 31) / 32, t2 = (d2 + 31) / 32;
+  int64_t id = blockIdx.x;
+  const int64_t ti2 = id % t2;
+  id /= t2;
+  const int64_t ti0 = id % t0;
+  id /= t0;
+  const int64_t j1 = id % b;
+  const int64_t r = id / b;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  const int64_t base0 = ti0 * 32, base2 = ti2 * 32;
+  if (TO_Y) {
+    // read blocks: i2 fastest (tx), i0 rows (ty)
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t i0 = base0 + k, i2 = base2 + tx;
+      if (i0 < a && i2 < d2) tile[k][tx] = src[((r * a + i0) * b + j1) * d2 + i2];
+    }
+    __syncthreads();
+    // write y: i0 fastest (tx), i2 rows (ty)
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t i2 = base2 + k, i0 = base0 + tx;
+      if (i0 < a && i2 < d2) dst[(j1 * d2 + i2) * d0 + r * a + i0] = tile[tx][k];
+    }
+  } else {
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t i2 = base2 + k, i0 = base0 + tx;
+      if (i0 < a && i2 < d2) tile[tx][k] = src[(j1 * d2 + i2) * d0 + r * a + i0];
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t i0 = base0 + k, i2 = base2 + tx;
+      if (i0 < a && i2 < d2) dst[((r * a + i0) * b + j1) * d2 + i2] = tile[k][tx];
+    }
+  }
+}
+
+int x_blocks(bool pack, int64_t a, int64_t d1, int64_t d2, int P, const double* src, double* dst,
+             cudaStream_t s) {
+  if (P < 1 || d1 % P || d2 % 2) return fail(FL_E_SHAPE, "slab transpose needs d1 % P == 0 and even d2");
+  const int64_t total = a * d1 * (d2 / 2);
+  const int grid = (int)std::min<int64_t>((total + T - 1) / T, 148 * 16);
+  if (pack) k_x_blocks<true><<<grid, T, 0, s>>>(a, d1, d2 / 2, P, (const double2*)src, (double2*)dst);
+  else k_x_blocks<false><<<grid, T, 0, s>>>(a, d1, d2 / 2, P, (const double2*)src, (double2*)dst);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+int y_blocks(bool to_y, int64_t a, int64_t b, int64_t d2, int P, const double* src, double* dst,
+             cudaStream_t s) {
+  if (P < 1) return fail(FL_E_SHAPE, "bad rank count");
+  const int64_t blocks = (int64_t)P * b * ((a + 31) / 32) * ((d2 + 31) / 32);
+  if (blocks > 0x7fffffffLL) return fail(FL_E_SHAPE, "slab too large");
+  if (to_y) k_y_blocks<true><<<(unsigned)blocks, T, 0, s>>>(a, b, d2, P, src, dst);
+  else k_y_blocks<false><<<(unsigned)blocks, T, 0, s>>>(a, b, d2, P, src, dst);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+}  // namespace
+}  // namespace fl
+
+using namespace fl;
+
+extern "C" {
+
+int fl_slab_pack_x(int64_t a, int64_t d1, int64_t d2, int nranks, const double* x_slab, double* send,
+                   fl_stream_t stream) {
+  if (!x_slab || !send) return fail(FL_E_VALUE, "null argument");
+  return x_blocks(true, a, d1, d2, nranks, x_slab, send, (cudaStream_t)stream);
+}
+
+int fl_slab_unpack_x(int64_t a, int64_t d1, int64_t d2, int nranks, const double* recv, double* x_slab,
+                     fl_stream_t stream) {
+  if (!x_slab || !recv) return fail(FL_E_VALUE, "null argument");
+  return x_blocks(false, a, d1, d2, nranks, recv, x_slab, (cudaStream_t)stream);
+}
+
+int fl_slab_unpack_y(int64_t a, int64_t b, int64_t d2, int nranks, const double* recv, double* y_slab,
+                     fl_stream_t stream) {
+  if (!y_slab || !recv) return fail(FL_E_VALUE, "null argument");
+  return y_blocks(true, a, b, d2, nranks, recv, y_slab, (cudaStream_t)stream);
+}
+
+int fl_slab_pack_y(int64_t a, int64_t b, int64_t d2, int nranks, const double* y_slab, double* send,
+                   fl_stream_t stream) {
+  if (!y_slab || !send) return fail(FL_E_VALUE, "null argument");
+  return y_blocks(false, a, b, d2, nranks, y_slab, send, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -8,6 +8,7 @@
 // not bitwise equal to NumPy/OpenBLAS summation.
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <string>
 
@@ -565,6 +566,46 @@ __global__ void k_pcg2_pupdate(int64_t n, const double* __restrict__ g1, const d
   emit(dq, SumOp(), red, partials, 0);
 }
 
+__global__ void k_pcg2_update_a(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
+                                double alpha, double* __restrict__ x, double* __restrict__ r,
+                                const double* __restrict__ p, const double* __restrict__ gp,
+                                double* __restrict__ partials) {
+  __shared__ double red[32];
+  double rho = 0.0;
+  GRID_LOOP(i, n) {
+    const double pt = p[i], pb = p[n + i];
+    const double a1 = g1[i], a2 = g2[i];
+    const double l1 = add(a1, a2), l2 = sub(a1, a2);
+    const double kt = add(add(gp[i], mul(l1, pt)), mul(l2, pb));
+    const double kb = add(mul(l2, pt), mul(l1, pb));
+    x[i] = add(x[i], mul(alpha, pt));
+    x[n + i] = add(x[n + i], mul(alpha, pb));
+    const double rt = sub(r[i], mul(alpha, kt));
+    const double rb = sub(r[n + i], mul(alpha, kb));
+    r[i] = rt;
+    r[n + i] = rb;
+    const Pinv P(a1, a2);
+    rho += mul(rt, P.top(rt, rb)) + mul(rb, P.bot(rt, rb));
+  }
+  emit(rho, SumOp(), red, partials, 0);
+}
+
+__global__ void k_objective_terms(int64_t n, const uint32_t* __restrict__ bits, const double* __restrict__ bhat,
+                                  const double* __restrict__ x, int64_t nb, const double* __restrict__ beta,
+                                  double* __restrict__ partials) {
+  __shared__ double red[32];
+  double ss = 0.0, l1 = 0.0;
+  GRID_LOOP(i, n) {
+    if (!((bits[i >> 5] >> (i & 31)) & 1u)) {
+      const double r = sub(bhat[i], x[i]);
+      ss += mul(r, r);
+    }
+  }
+  if (beta) GRID_LOOP(i, nb) l1 += fabs(beta[i]);
+  emit(ss, SumOp(), red, partials, 0);
+  emit(l1, SumOp(), red, partials, 1);
+}
+
 // Reduce ``nk`` partial rows and fetch them to the host.
 int reduce_fetch(Scratch* sc, int grid, int nk, const int* kinds, double* out, cudaStream_t s) {
   FL_TRY(finish_reduce(sc->partials, grid, nk, kinds, sc->result, s));
@@ -914,6 +955,56 @@ int fl_xpby(int64_t n, const double* x, double beta, double* y, fl_stream_t stre
   k_xpby<<<grid_for(n, T), T, 0, (cudaStream_t)stream>>>(n, x, beta, y);
   FL_LAUNCH_CHECK();
   return FL_OK;
+}
+
+int fl_pcg_step_init(int64_t n, const double* sigma1, const double* sigma2, const double* rhs, double* x,
+                     double* r, double* p, double* out, fl_stream_t stream) {
+  if (!sigma1 || !sigma2 || !rhs || !x || !r || !p || !out) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  int grid = 0;
+  FL_TRY(pcg2_init(n, sigma1, sigma2, rhs, x, r, p, sc->partials, &grid, s));
+  const int kinds[2] = {RED_SUM, RED_SUM};
+  return reduce_fetch(sc, grid, 2, kinds, out, s);
+}
+
+int fl_pcg_step_update(int64_t n, const double* sigma1, const double* sigma2, double alpha, double* x, double* r,
+                       const double* p, const double* g, double* out, fl_stream_t stream) {
+  if (!sigma1 || !sigma2 || !x || !r || !p || !g || !out) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  const int grid = grid_for(n, T);
+  k_pcg2_update_a<<<grid, T, 0, s>>>(n, sigma1, sigma2, alpha, x, r, p, g, sc->partials);
+  FL_LAUNCH_CHECK();
+  const int kind = RED_SUM;
+  return reduce_fetch(sc, grid, 1, &kind, out, s);
+}
+
+int fl_pcg_step_pupdate(int64_t n, const double* sigma1, const double* sigma2, const double* r, double beta,
+                        double* p, double* out, fl_stream_t stream) {
+  if (!sigma1 || !sigma2 || !r || !p || !out) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  int grid = 0;
+  FL_TRY(pcg2_pupdate(n, sigma1, sigma2, r, beta, p, sc->partials, &grid, s));
+  const int kind = RED_SUM;
+  return reduce_fetch(sc, grid, 1, &kind, out, s);
+}
+
+int fl_objective_terms(int64_t n, const uint32_t* bits, const double* bhat, const double* x, int64_t n_beta,
+                       const double* beta, double* out, fl_stream_t stream) {
+  if (!bits || !bhat || !x || !out) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  const int grid = grid_for(std::max(n, n_beta), T);
+  k_objective_terms<<<grid, T, 0, s>>>(n, bits, bhat, x, n_beta, beta, sc->partials);
+  FL_LAUNCH_CHECK();
+  const int kinds[2] = {RED_SUM, RED_SUM};
+  return reduce_fetch(sc, grid, 2, kinds, out, s);
 }
 
 }  // extern "C"
