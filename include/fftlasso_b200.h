@@ -180,6 +180,13 @@ FL_API int fl_kkt_apply_profiled(fl_plan_t plan, const uint32_t* miss_bits, cons
                                  const double* sigma2, const double* d_beta, const double* d_z,
                                  double* top, double* bottom, double* pass_ms, int* npasses,
                                  fl_stream_t stream);
+/* KKT epilogue alone on a gram output g (in place -> top):
+ * top = (g + L1 d_beta) + L2 d_z, bottom = L2 d_beta + L1 d_z
+ * (newton_system.py:150-151); optional LOCAL d.Kd to the host (synchronises).
+ * Used by the slab-sharded matvec after the sharded gram. */
+FL_API int fl_kkt_epilogue(int64_t n, double* g_top, const double* d_beta, const double* d_z,
+                           const double* sigma1, const double* sigma2, double* bottom,
+                           double* pkp_host, fl_stream_t stream);
 /* apply_precond_inverse (newton_system.py:155-159). */
 FL_API int fl_precond_apply(int64_t n, const double* sigma1, const double* sigma2, const double* r_beta,
                      const double* r_c, double* top, double* bottom, fl_stream_t stream);

@@ -289,6 +289,24 @@ int fl_kkt_apply(fl_plan_t p, const uint32_t* bits, const double* sigma1, const 
   return FL_OK;
 }
 
+int fl_kkt_epilogue(int64_t n, double* g, const double* d_beta, const double* d_z, const double* sigma1,
+                    const double* sigma2, double* bottom, double* pkp_host, fl_stream_t stream) {
+  if (!g || !d_beta || !d_z || !sigma1 || !sigma2) return fail(FL_E_VALUE, "null argument");
+  if (n % 2) return fail(FL_E_SHAPE, "epilogue needs an even length");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  int nb = 0;
+  FL_TRY(kkt_epilogue(n, g, d_beta, d_z, sigma1, sigma2, bottom, pkp_host ? sc->partials : nullptr, &nb, s));
+  if (pkp_host) {
+    const int kind = RED_SUM;
+    FL_TRY(finish_reduce(sc->partials, nb, 1, &kind, sc->result, s));
+    FL_TRY(fetch_results(sc, 1, s));
+    *pkp_host = sc->host[0];
+  }
+  return FL_OK;
+}
+
 int fl_kkt_apply_profiled(fl_plan_t p, const uint32_t* bits, const double* sigma1,
                           const double* sigma2, const double* d_beta, const double* d_z, double* top,
                           double* bottom, double* pass_ms, int* npasses, fl_stream_t stream) {

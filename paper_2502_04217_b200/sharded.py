@@ -1,0 +1,501 @@
+"""Slab-sharded 3D operators and IPM solve over P ranks.
+
+Layout (d0 = P a, d1 = P b, all dims even):
+
+* **X-slab** of rank r: rows i0 in [r a, (r+1) a), local shape (a, d1, d2) --
+  a contiguous chunk of the global row-major vector.  Every IPM / PCG vector
+  lives in X-slabs, so all elementwise work is local.
+* **Y-slab** of rank r: i1 in [r b, (r+1) b), local layout (b, d2, d0) -- axis 0
+  is local *and contiguous*, so the fused synth/mask/analysis pass of the
+  single-GPU path runs unchanged on it.  The mask bits and b_hat are stored
+  in this layout.
+
+gram (masking.py:107-118; the per-axis maps commute, fourier.py:14-16):
+
+    X: synth axis 2, synth axis 1  ->  all-to-all X->Y  ->
+    Y: synth axis 0 . Z . analyze axis 0 (one fused pass)  ->  all-to-all Y->X  ->
+    X: analyze axis 1, analyze axis 2
+
+i.e. the single-GPU pass count (5) plus two transposes.  Scalars (dots, norms,
+maxima, minima) are combined with one all-reduce per decision point.
+
+``Comm`` hides the exchange: ``DistComm`` runs one shard per process over
+``torch.distributed`` (NCCL on B200s; gloo on CPU), ``LocalComm`` holds all
+P shards of a grid in one process (single-GPU emulation of the sharded
+algorithm -- no kernel ever waits on another rank).  Every operation below
+works on *lists of local shards* (length 1 under DistComm, P under
+LocalComm).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev, _lib
+from .errors import NumericalBreakdownError, StalledError, UnsupportedShapeError
+from .ipm import FIELDS, IpmConfig, IpmState, IterationRecord, SolveReport, _alpha_from_ratio, next_barrier
+from .newton_system import fl_state
+from .pcg import PcgConfig
+
+SUM, MAX, MIN = "sum", "max", "min"
+
+
+# ---------------------------------------------------------------------------
+# geometry and communication
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class SlabGeometry:
+    dims: tuple
+    P: int
+
+    def __post_init__(self):
+        d0, d1, d2 = self.dims
+        if any(d < 2 or d % 2 for d in self.dims):
+            raise UnsupportedShapeError("every axis must be even and >= 2")
+        if d0 % self.P or d1 % self.P:
+            raise UnsupportedShapeError(f"slab sharding needs d0 and d1 divisible by P={self.P}")
+
+    @property
+    def a(self):
+        return self.dims[0] // self.P
+
+    @property
+    def b(self):
+        return self.dims[1] // self.P
+
+    @property
+    def n_local(self):
+        return self.dims[0] * self.dims[1] * self.dims[2] // self.P
+
+    @property
+    def n(self):
+        return self.dims[0] * self.dims[1] * self.dims[2]
+
+    # host-side layout helpers (input scatter / result gather, tests)
+    def x_slab(self, full: np.ndarray, r: int) -> np.ndarray:
+        return full.reshape(-1)[r * self.n_local:(r + 1) * self.n_local]
+
+    def y_slab(self, full: np.ndarray, r: int) -> np.ndarray:
+        d0, d1, d2 = self.dims
+        g = full.reshape(d0, d1, d2)[:, r * self.b:(r + 1) * self.b, :]  # (d0, b, d2)
+        return np.ascontiguousarray(np.transpose(g, (1, 2, 0))).reshape(-1)  # (b, d2, d0)
+
+    def from_x(self, slabs) -> np.ndarray:
+        return np.concatenate([np.asarray(s).reshape(-1) for s in slabs])
+
+
+class Comm:
+    """Exchange interface over the shards held by this process."""
+
+    world: int
+    ranks: list  # global rank of each local shard
+
+    def all_to_all(self, send: list) -> list:
+        raise NotImplementedError
+
+    def reduce(self, values: list, op: str) -> np.ndarray:
+        raise NotImplementedError
+
+
+class LocalComm(Comm):
+    """All P shards in this process: exchanges are block copies."""
+
+    def __init__(self, P: int):
+        self.world = P
+        self.ranks = list(range(P))
+
+    def all_to_all(self, send):
+        P = self.world
+        blk = send[0].numel() // P
+        recv = [s.new_empty(s.shape) for s in send]
+        for dst in range(P):
+            for src in range(P):
+                recv[dst][src * blk:(src + 1) * blk].copy_(send[src][dst * blk:(dst + 1) * blk])
+        return recv
+
+    def reduce(self, values, op):
+        arr = np.array([np.asarray(v, dtype=np.float64).reshape(-1) for v in values])
+        return {SUM: arr.sum(0), MAX: arr.max(0), MIN: arr.min(0)}[op]
+
+
+class DistComm(Comm):
+    """One shard per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.ranks = [dist.get_rank(group)]
+        self.device = device
+
+    def all_to_all(self, send):
+        (s,) = send
+        recv = s.new_empty(s.shape)
+        self.dist.all_to_all_single(recv, s, group=self.group)
+        return [recv]
+
+    def reduce(self, values, op):
+        import torch
+
+        (v,) = values
+        t = torch.as_tensor(np.asarray(v, dtype=np.float64).reshape(-1),
+                            device=self.device if self.device is not None else "cpu")
+        rop = {SUM: self.dist.ReduceOp.SUM, MAX: self.dist.ReduceOp.MAX, MIN: self.dist.ReduceOp.MIN}[op]
+        self.dist.all_reduce(t, op=rop, group=self.group)
+        return t.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# local device operations of one shard (C ABI)
+# ---------------------------------------------------------------------------
+
+class ShardOps:
+    """Per-shard GPU kernels: X-slab passes, Y-slab fused pass, slab transposes."""
+
+    def __init__(self, geo: SlabGeometry):
+        self.geo = geo
+        d0, d1, d2 = geo.dims
+        dev = _dev.device().index
+        self.x_plan = self._plan((geo.a, d1, d2), 0b110, dev)
+        self.y_plan = self._plan((geo.b, d2, d0), 0b100, dev)
+
+    @staticmethod
+    def _plan(dims, mask, dev):
+        arr = (ctypes.c_int64 * 3)(*dims)
+        h = ctypes.c_void_p()
+        _lib.call("fl_plan_create_ex", 3, arr, mask, dev, ctypes.byref(h))
+        return h
+
+    # buffers of this backend
+    @staticmethod
+    def empty(n):
+        return _dev.empty(n)
+
+    @staticmethod
+    def vec(a):
+        return _dev.to_dev(a)
+
+    @staticmethod
+    def bits(flags):
+        import torch
+
+        return torch.from_numpy(pack_bits(flags)).to(_dev.device())
+
+    def close(self):
+        for h in (self.x_plan, self.y_plan):
+            if h:
+                _lib.lib().fl_plan_destroy(h)
+        self.x_plan = self.y_plan = None
+
+    def synth_x(self, src, dst):  # axes 2 then 1 of the X-slab
+        _lib.call("fl_axis_pass", self.x_plan, 2, 0, _dev.ptr(src), _dev.ptr(dst), _dev.stream())
+        _lib.call("fl_axis_pass", self.x_plan, 1, 0, _dev.ptr(dst), _dev.ptr(dst), _dev.stream())
+
+    def analyze_x(self, src, dst):
+        _lib.call("fl_axis_pass", self.x_plan, 1, 1, _dev.ptr(src), _dev.ptr(dst), _dev.stream())
+        _lib.call("fl_axis_pass", self.x_plan, 2, 1, _dev.ptr(dst), _dev.ptr(dst), _dev.stream())
+
+    def synth_y0(self, src, dst):  # axis 0 of the grid = contiguous axis of the Y-slab
+        _lib.call("fl_axis_pass", self.y_plan, 2, 0, _dev.ptr(src), _dev.ptr(dst), _dev.stream())
+
+    def fused_y(self, bits, bhat, src, dst, want_norm: bool):
+        nrm = ctypes.c_double(0.0)
+        _lib.call("fl_fused_mask_pass", self.y_plan, _dev.ptr(bits), _dev.ptr(bhat) if bhat is not None else None,
+                  _dev.ptr(src), _dev.ptr(dst), ctypes.byref(nrm) if want_norm else None, _dev.stream())
+        return nrm.value
+
+    def pack_x(self, x, send):
+        g = self.geo
+        _lib.call("fl_slab_pack_x", g.a, g.dims[1], g.dims[2], g.P, _dev.ptr(x), _dev.ptr(send), _dev.stream())
+
+    def unpack_y(self, recv, y):
+        g = self.geo
+        _lib.call("fl_slab_unpack_y", g.a, g.b, g.dims[2], g.P, _dev.ptr(recv), _dev.ptr(y), _dev.stream())
+
+    def pack_y(self, y, send):
+        g = self.geo
+        _lib.call("fl_slab_pack_y", g.a, g.b, g.dims[2], g.P, _dev.ptr(y), _dev.ptr(send), _dev.stream())
+
+    def unpack_x(self, recv, x):
+        g = self.geo
+        _lib.call("fl_slab_unpack_x", g.a, g.dims[1], g.dims[2], g.P, _dev.ptr(recv), _dev.ptr(x), _dev.stream())
+
+
+# ---------------------------------------------------------------------------
+# sharded operators
+# ---------------------------------------------------------------------------
+
+class ShardedGrid:
+    """Geometry, comm, per-shard ops and exchange buffers of one sharded grid."""
+
+    def __init__(self, dims, comm: Comm, ops_factory=ShardOps):
+        self.geo = SlabGeometry(tuple(int(d) for d in dims), comm.world)
+        self.comm = comm
+        self.ops = [ops_factory(self.geo) for _ in comm.ranks]
+        n = self.geo.n_local
+        self.send = [self.ops[0].empty(n) for _ in comm.ranks]
+        self.ybuf = [self.ops[0].empty(n) for _ in comm.ranks]
+
+    def x_to_y(self, xs, ys):
+        for op, x, s in zip(self.ops, xs, self.send):
+            op.pack_x(x, s)
+        recv = self.comm.all_to_all(self.send)
+        for op, rv, y in zip(self.ops, recv, ys):
+            op.unpack_y(rv, y)
+
+    def y_to_x(self, ys, xs):
+        for op, y, s in zip(self.ops, ys, self.send):
+            op.pack_y(y, s)
+        recv = self.comm.all_to_all(self.send)
+        for op, rv, x in zip(self.ops, recv, xs):
+            op.unpack_x(rv, x)
+
+    def synthesize_to_y(self, betas, ys):
+        """A beta with beta in X-slabs; result in Y-slabs (b, d2, d0)."""
+        for op, b, y in zip(self.ops, betas, self.ybuf):
+            op.synth_x(b, y)  # ybuf used as X-layout scratch here
+        self.x_to_y(self.ybuf, ys)
+        for op, y in zip(self.ops, ys):
+            op.synth_y0(y, y)
+
+    def gram(self, betas, outs, bits_y, bhat_y=None, want_norm=False):
+        """outs = A^T Z A beta (bhat_y None) or A^T Z (b_hat - A beta); X-slabs in/out.
+
+        Returns the all-reduced ||Z A beta||^2 when ``want_norm`` (gram only).
+        """
+        for op, b, o in zip(self.ops, betas, outs):
+            op.synth_x(b, o)
+        self.x_to_y(outs, self.ybuf)
+        norms = []
+        for i, (op, y) in enumerate(zip(self.ops, self.ybuf)):
+            norms.append(op.fused_y(bits_y[i], None if bhat_y is None else bhat_y[i], y, y, want_norm))
+        self.y_to_x(self.ybuf, outs)
+        for op, o in zip(self.ops, outs):
+            op.analyze_x(o, o)
+        if want_norm:
+            return float(self.comm.reduce([[v] for v in norms], SUM)[0])
+        return None
+
+
+# ---------------------------------------------------------------------------
+# sharded IPM solve (ipm.py:402-486 over slabs)
+# ---------------------------------------------------------------------------
+
+def _st(st):
+    return ctypes.byref(fl_state(st))
+
+
+class ShardedProblem:
+    """Per-shard device data of one instance: Y-layout mask bits and b_hat."""
+
+    def __init__(self, grid: ShardedGrid, bits_y, bhat_y):
+        self.grid = grid
+        self.bits_y = bits_y
+        self.bhat_y = bhat_y
+
+    @classmethod
+    def from_host(cls, grid: ShardedGrid, flags: np.ndarray, b_hat_full: np.ndarray):
+        """Scatter a host problem (full-grid missing flags, embedded b) to this process's shards."""
+        bits, bh = [], []
+        for r in grid.comm.ranks:
+            bits.append(grid.ops[0].bits(grid.geo.y_slab(np.asarray(flags, dtype=np.uint8), r)))
+            bh.append(grid.ops[0].vec(grid.geo.y_slab(np.asarray(b_hat_full, dtype=np.float64), r)))
+        return cls(grid, bits, bh)
+
+
+def pack_bits(flags: np.ndarray) -> np.ndarray:
+    """Missing flags -> little-endian 32-bit words (bit v & 31 of word v >> 5)."""
+    pad = (-flags.size) % 32
+    fb = np.concatenate([np.asarray(flags, dtype=np.uint8).reshape(-1), np.zeros(pad, np.uint8)])
+    return np.packbits(fb, bitorder="little").view(np.int32).copy()
+
+
+def sharded_solve(prob: ShardedProblem, lam: float, config: IpmConfig = IpmConfig(), observer=None):
+    """Interior-point solve over slabs; returns (beta X-slabs, SolveReport).
+
+    Same control flow, scalars and records as ipm.solve; every scalar decision
+    uses one all-reduce of the local kernel reductions.
+    """
+    grid = prob.grid
+    comm = grid.comm
+    nl = grid.geo.n_local
+    n = grid.geo.n
+    S = len(comm.ranks)
+    L = _lib.lib()
+    s = _dev.stream()
+    ws = [_Work(nl) for _ in range(S)]
+    mu = lam / 2.0 if config.mu_init is None else float(config.mu_init)
+    for w in ws:
+        _lib.check(L.fl_ipm_init(nl, _st(w.state), float(lam), s))
+
+    def resid():
+        grid.gram([w.state.beta for w in ws], [w.g for w in ws], prob.bits_y, prob.bhat_y)
+
+    def assess(mu_):
+        vals = []
+        for w in ws:
+            a = _lib.FlAssess()
+            _lib.check(L.fl_ipm_assess(nl, _st(w.state), _dev.ptr(w.g), float(lam), float(mu_), ctypes.byref(a), s))
+            vals.append([a.stationarity, a.dual_equality, a.multiplier_gap, a.primal, a.complementarity,
+                         a.barrier_residual, a.min_product, a.dot_nu_s1, a.dot_nu_s2])
+        mx = comm.reduce([v[:6] for v in vals], MAX)
+        mn = comm.reduce([v[6:7] for v in vals], MIN)
+        sm = comm.reduce([v[7:9] for v in vals], SUM)
+        worst = max(mx[:5])
+        measure = float(sm[0] + sm[1]) / (2 * n)
+        return dict(stationarity=mx[0], dual_equality=mx[1], multiplier_gap=mx[2], primal=mx[3],
+                    complementarity=mx[4], max_residual=worst, converged=worst <= config.tol,
+                    centrality_ok=bool(mn[0] >= config.gamma_centrality * measure),
+                    barrier_residual=mx[5], duality_measure=measure)
+
+    t0 = time.perf_counter()
+    records = []
+    best_kkt = math.inf
+    for w in ws:
+        w.best.copy_(w.state.beta)
+    status = "max_iters"
+    resid()
+    conv = assess(mu)
+    for iteration in range(1, config.max_iters + 1):
+        if conv["converged"]:
+            status = "converged"
+            break
+        if conv["barrier_residual"] <= config.inner_slack * mu:
+            mu = next_barrier(mu, config.tol, config)
+        t_iter = time.perf_counter()
+        bad = []
+        for w in ws:
+            st = L.fl_barrier_diagonals(nl, *(_dev.ptr(getattr(w.state, f)) for f in ("s1", "s2", "nu1", "nu2")),
+                                        _dev.ptr(w.sig1), _dev.ptr(w.sig2), None, None, None, None, s)
+            bad.append([0.0 if st == 0 else 1.0])
+            if st not in (0, _lib.FL_E_INTERIOR):
+                _lib.check(st)
+            _lib.check(L.fl_newton_rhs(nl, _st(w.state), _dev.ptr(w.g), _dev.ptr(w.sig1), _dev.ptr(w.sig2),
+                                       float(lam), float(mu), None, None, None, None, None, None,
+                                       _dev.ptr(w.rhs[:nl]), _dev.ptr(w.rhs[nl:]), s))
+        if comm.reduce(bad, MAX)[0]:
+            from .errors import InteriorViolationError
+            raise InteriorViolationError("slacks and multipliers must be strictly positive and finite")
+        iters, res_norm = _sharded_pcg(grid, prob, ws, PcgConfig(abs_tol=config.cg_tol, max_iters=config.cg_max_iters))
+        tau = max(config.ftb_tau, 1.0 - mu)
+        ratios = []
+        for w in ws:
+            rr = (ctypes.c_double * 4)()
+            _lib.check(L.fl_ipm_ratios(nl, _st(w.state), _dev.ptr(w.sig1), _dev.ptr(w.sig2), float(mu),
+                                       _dev.ptr(w.x[:nl]), _dev.ptr(w.x[nl:]), rr, s))
+            ratios.append(list(rr))
+        rmin = comm.reduce(ratios, MIN)
+        alpha_p = min(_alpha_from_ratio(rmin[0], tau), _alpha_from_ratio(rmin[1], tau))
+        alpha_d = min(_alpha_from_ratio(rmin[2], tau), _alpha_from_ratio(rmin[3], tau))
+        if min(alpha_p, alpha_d) < 1e-12:
+            raise StalledError(f"fraction-to-boundary step collapsed (alpha_p={alpha_p:.2e}, alpha_d={alpha_d:.2e})")
+        stalled = []
+        for w in ws:
+            st = L.fl_ipm_update(nl, _st(w.state), _dev.ptr(w.sig1), _dev.ptr(w.sig2), float(mu),
+                                 _dev.ptr(w.x[:nl]), _dev.ptr(w.x[nl:]), float(alpha_p), float(alpha_d), s)
+            if st not in (0, _lib.FL_E_STALLED):
+                _lib.check(st)
+            stalled.append([1.0 if st == _lib.FL_E_STALLED else 0.0])
+        if comm.reduce(stalled, MAX)[0]:
+            raise StalledError("slack or multiplier left the strict interior")
+        resid()
+        conv = assess(mu)
+        rec = IterationRecord(iteration=iteration, mu=mu, primal_inf=conv["primal"],
+                              dual_inf=max(conv["dual_equality"], conv["multiplier_gap"], conv["stationarity"]),
+                              complementarity=conv["complementarity"], kkt_max=conv["max_residual"],
+                              krylov_iters=iters, alpha_primal=alpha_p, alpha_dual=alpha_d,
+                              pcg_residual=res_norm, centrality_ok=conv["centrality_ok"],
+                              wall_time=time.perf_counter() - t_iter)
+        records.append(rec)
+        if conv["max_residual"] < best_kkt:
+            best_kkt = conv["max_residual"]
+            for w in ws:
+                w.best.copy_(w.state.beta)
+        if observer is not None:
+            observer([w.state for w in ws], rec)
+    else:
+        if conv["converged"]:
+            status = "converged"
+    betas = [w.state.beta if status == "converged" else w.best for w in ws]
+    # objective: x = A beta in Y-slabs against b_hat / mask in the same layout
+    terms = []
+    for w in ws:
+        w.g.zero_()
+    grid.synthesize_to_y(betas, [w.g for w in ws])
+    for i, w in enumerate(ws):
+        out = (ctypes.c_double * 2)()
+        _lib.check(L.fl_objective_terms(nl, _dev.ptr(prob.bits_y[i]), _dev.ptr(prob.bhat_y[i]), _dev.ptr(w.g), nl,
+                                        _dev.ptr(betas[i]), out, s))
+        terms.append([out[0], out[1]])
+    t = comm.reduce(terms, SUM)
+    report = SolveReport(status=status, iterations=len(records), lam=lam, tol=config.tol, records=records,
+                         final_objective=0.5 * float(t[0]) + lam * float(t[1]),
+                         final_kkt=conv["max_residual"] if status == "converged" else best_kkt,
+                         final_mu=mu, wall_time=time.perf_counter() - t0)
+    return betas, report
+
+
+class _Work:
+    def __init__(self, nl):
+        self.state = IpmState(mu=0.0, **{f: _dev.empty(nl) for f in FIELDS})
+        self.sig1, self.sig2, self.g, self.best = (_dev.empty(nl) for _ in range(4))
+        self.rhs, self.x, self.r, self.p = (_dev.empty(2 * nl) for _ in range(4))
+        self.gp = _dev.empty(nl)
+
+
+def _sharded_pcg(grid: ShardedGrid, prob: ShardedProblem, ws, cfg: PcgConfig):
+    """PCG v2 over slabs (pcg.py:57-127): curvature = ||Z A p_beta||^2 + diagonal form."""
+    comm = grid.comm
+    nl = grid.geo.n_local
+    L = _lib.lib()
+    s = _dev.stream()
+    limit = cfg.iteration_limit(2 * grid.geo.n)
+    parts = []
+    for w in ws:
+        out = (ctypes.c_double * 2)()
+        _lib.check(L.fl_pcg_step_init(nl, _dev.ptr(w.sig1), _dev.ptr(w.sig2), _dev.ptr(w.rhs), _dev.ptr(w.x),
+                                      _dev.ptr(w.r), _dev.ptr(w.p), out, s))
+        parts.append([out[0], out[1]])
+    rho, dq = comm.reduce(parts, SUM)
+    if not math.isfinite(rho) or rho < 0:
+        raise NumericalBreakdownError(f"preconditioner produced r'P^{{-1}}r = {rho}")
+    norm = math.sqrt(rho)
+    thr = cfg.abs_tol + cfg.rel_tol * norm
+    if norm <= thr:
+        return 0, norm
+    for k in range(1, limit + 1):
+        curv_g = grid.gram([w.p[:nl] for w in ws], [w.gp for w in ws], prob.bits_y, want_norm=True)
+        curv = curv_g + dq
+        if not math.isfinite(curv) or curv <= 0:
+            raise NumericalBreakdownError(f"nonpositive curvature p'Kp = {curv} at iteration {k}")
+        alpha = rho / curv
+        parts = []
+        for w in ws:
+            out = ctypes.c_double()
+            _lib.check(L.fl_pcg_step_update(nl, _dev.ptr(w.sig1), _dev.ptr(w.sig2), float(alpha), _dev.ptr(w.x),
+                                            _dev.ptr(w.r), _dev.ptr(w.p), _dev.ptr(w.gp), ctypes.byref(out), s))
+            parts.append([out.value])
+        rho_next = float(comm.reduce(parts, SUM)[0])
+        if not math.isfinite(rho_next) or rho_next < 0:
+            raise NumericalBreakdownError(f"r'P^{{-1}}r = {rho_next} at iteration {k}")
+        norm = math.sqrt(rho_next)
+        if norm <= thr:
+            return k, norm
+        beta = rho_next / rho
+        parts = []
+        for w in ws:
+            out = ctypes.c_double()
+            _lib.check(L.fl_pcg_step_pupdate(nl, _dev.ptr(w.sig1), _dev.ptr(w.sig2), _dev.ptr(w.r), float(beta),
+                                             _dev.ptr(w.p), ctypes.byref(out), s))
+            parts.append([out.value])
+        dq = float(comm.reduce(parts, SUM)[0])
+        rho = rho_next
+    raise NumericalBreakdownError(f"PCG stalled at preconditioned residual {norm:.3e} after {limit} iterations")

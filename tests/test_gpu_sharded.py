@@ -1,0 +1,75 @@
+"""GPU: slab-sharded operators and solve with P emulated ranks on one GPU.
+
+LocalComm keeps all P shards in one process (no kernel waits on another
+rank), so the CUDA slab transposes, the X-slab passes and the Y-slab fused
+pass are checked against the oracle on the full grid, and the sharded IPM
+solve against the single-GPU solve.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import fftlasso_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+fl = pytest.importorskip("paper_2502_04217_b200")
+from paper_2502_04217_b200 import sharded as sh  # noqa: E402
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("dims", [(8, 8, 16), (16, 32, 64), (64, 64, 64), (128, 32, 512)])
+def test_sharded_operators_match_oracle(P, dims):
+    if dims[0] % P or dims[1] % P:
+        pytest.skip("not divisible")
+    comm = sh.LocalComm(P)
+    grid = sh.ShardedGrid(dims, comm)
+    geo = grid.geo
+    rng = np.random.default_rng(P * 1000 + dims[2])
+    beta = rng.standard_normal(geo.n)
+    flags = rng.random(geo.n) < 0.15
+    bfull = rng.standard_normal(geo.n)
+    om = orc.make_mask(dims, flags=flags)
+    prob = sh.ShardedProblem.from_host(grid, flags, np.where(flags, 0.0, bfull))
+    xb = [fl._dev.to_dev(geo.x_slab(beta, r)) for r in comm.ranks]
+    g = [fl._dev.empty(geo.n_local) for _ in comm.ranks]
+    nrm = grid.gram(xb, g, prob.bits_y, want_norm=True)
+    ref = orc.gram(beta, om)
+    got = geo.from_x([t.cpu().numpy() for t in g])
+    tol = 1e-12 * np.abs(beta).max()
+    assert np.max(np.abs(got - ref)) <= tol
+    ax = orc.synthesize(beta, dims)
+    assert abs(nrm - np.sum(ax[~flags] ** 2)) <= 1e-12 * nrm
+    grid.gram(xb, g, prob.bits_y, prob.bhat_y)
+    ref_r = orc.observe_adjoint(bfull[~flags] - orc.observe(beta, om), om)
+    assert np.max(np.abs(geo.from_x([t.cpu().numpy() for t in g]) - ref_r)) <= 1e-12 * np.abs(ref_r).max()
+    ys = [fl._dev.empty(geo.n_local) for _ in comm.ranks]
+    grid.synthesize_to_y(xb, ys)
+    for r in comm.ranks:
+        assert np.max(np.abs(ys[r].cpu().numpy() - geo.y_slab(ax, r))) <= tol
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_solve_matches_single_gpu(P):
+    g = load_golden("solve_c4_32")
+    dims = tuple(int(d) for d in g["dims"])
+    mask = fl.Mask(g["missing"], fl.GridShape(dims))
+    lam = float(g["lam"])
+    beta1, rep1 = fl.solve(g["b"], mask, fl.IpmConfig(lam=lam))
+    comm = sh.LocalComm(P)
+    grid = sh.ShardedGrid(dims, comm)
+    bhat = np.zeros(mask.shape.n)
+    bhat[~mask.missing_bool] = g["b"]
+    prob = sh.ShardedProblem.from_host(grid, mask.missing_bool, bhat)
+    betas, rep = sh.sharded_solve(prob, lam, fl.IpmConfig(lam=lam))
+    beta = grid.geo.from_x([t.cpu().numpy() for t in betas])
+    assert rep.status == rep1.status == "converged"
+    assert rep.iterations == rep1.iterations
+    assert all(abs(a - b) <= 1 for a, b in zip(rep.krylov_counts, rep1.krylov_counts))
+    assert abs(rep.final_objective - rep1.final_objective) <= 1e-9 * abs(rep1.final_objective)
+    assert np.linalg.norm(beta - beta1) <= 1e-8 * np.linalg.norm(beta1)
+    ref = [r["krylov_iters"] for r in json.loads(str(g["records_json"]))]
+    assert abs(rep.iterations - len(ref)) <= 1
