@@ -285,6 +285,36 @@ class ShardedGrid:
         return None
 
 
+def kkt_apply(grid: ShardedGrid, bits_y, sig1, sig2, d_betas, d_zs, tops, bots, want_pkp=False):
+    """Sharded condensed KKT matvec (newton_system.py:148-152) on X-slabs.
+
+    Sharded gram, then the local elementwise epilogue on every slab; returns
+    the all-reduced d.Kd when ``want_pkp``.
+    """
+    grid.gram(d_betas, tops, bits_y)
+    L = _lib.lib()
+    parts = []
+    for i, (t, b, db, dz) in enumerate(zip(tops, bots, d_betas, d_zs)):
+        v = ctypes.c_double()
+        _lib.check(L.fl_kkt_epilogue(grid.geo.n_local, _dev.ptr(t), _dev.ptr(db), _dev.ptr(dz), _dev.ptr(sig1[i]),
+                                     _dev.ptr(sig2[i]), _dev.ptr(b), ctypes.byref(v) if want_pkp else None,
+                                     _dev.stream()))
+        parts.append([v.value])
+    return float(grid.comm.reduce(parts, SUM)[0]) if want_pkp else None
+
+
+def bragg_y_flags(geo: SlabGeometry, r: int, spacing: int = 16, radius: float = 5.3) -> np.ndarray:
+    """Bragg punch mask (workloads.bragg_flags) generated directly in rank r's
+    Y-slab layout (b, d2, d0) -- no full-grid host array for C5-sized grids."""
+    d0, d1, d2 = geo.dims
+    def sq(m):
+        t = np.arange(m) % spacing
+        return np.minimum(t, spacing - t).astype(np.int64) ** 2
+    s0, s1, s2 = sq(d0), sq(d1)[r * geo.b:(r + 1) * geo.b], sq(d2)
+    tot = s1[:, None, None] + s2[None, :, None] + s0[None, None, :]
+    return (tot <= radius * radius).reshape(-1)
+
+
 # ---------------------------------------------------------------------------
 # sharded IPM solve (ipm.py:402-486 over slabs)
 # ---------------------------------------------------------------------------
