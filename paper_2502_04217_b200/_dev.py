@@ -69,8 +69,17 @@ def zeros(n: int):
 
 
 def out(t, like_host: bool):
-    """Return ``t`` as NumPy when the caller passed host data."""
-    return t.cpu().numpy() if like_host else t
+    """Return ``t`` as NumPy when the caller passed host data.
+
+    The device->host copy lands in page-locked memory from torch's caching
+    host allocator (full-bandwidth DMA; freed results are recycled by later
+    calls), exposed to the caller as a NumPy view.
+    """
+    if not like_host:
+        return t
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
 
 
 class Plan:
