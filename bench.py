@@ -254,15 +254,19 @@ def run_b200(args, rank: int, world: int):
     h_db.copy_(d[:n])
     h_dz.copy_(d[n:])
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    apply_kkt(h_db, h_dz, diag, mask)
+    checksum = 0.0
+    for _ in range(2):  # warm the pinned host-allocator cache
+        out_top, out_bot = apply_kkt(h_db, h_dz, diag, mask)
+        del out_top, out_bot
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        out_top, out_bot = apply_kkt(h_db, h_dz, diag, mask)  # returns host arrays
+        out_top, out_bot = apply_kkt(h_db, h_dz, diag, mask)  # returns host (NumPy) arrays
+        checksum += float(out_top[0]) + float(out_bot[-1])  # consume, then drop
+        del out_top, out_bot
     barrier()
     e2e_s = time.perf_counter() - t0
-    assert out_top.shape == (n,)
-    del out_top, out_bot, h_db, h_dz
+    del h_db, h_dz
     e2e = {"value": round(world * e2e_steps / e2e_s, 3), "unit": UNIT,
            "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": 2 * n * 8,
            "steps": e2e_steps, "api": "newton_system.apply_kkt(pinned host d_beta, d_z)"}
