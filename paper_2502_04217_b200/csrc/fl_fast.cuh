@@ -34,13 +34,15 @@ constexpr int imax(int a, int b) { return a > b ? a : b; }
 //        1 -> one cp.async staging buffer, refilled with the next tile as
 //             soon as the current tile has been read out of it,
 //        2 -> two staging buffers (double buffering).
-constexpr int cfg_code(int t_sel, int pipe, int mb) { return t_sel * 9 + pipe * 3 + (mb - 1); }
+constexpr int cfg_code(int t_sel, int pipe, int mb, int e16 = 0) {
+  return e16 * 27 + t_sel * 9 + pipe * 3 + (mb - 1);
+}
 
 template <int M, int CFG = 0>
 struct Geom {
-  static constexpr int E = M >= 1024 ? 16 : 8;                  // elements per thread
+  static constexpr int E = (M >= 1024 || CFG >= 27) ? 16 : 8;   // elements per thread
   static constexpr int P = M / E;                               // threads per fibre
-  static constexpr int T_SEL = CFG / 9;
+  static constexpr int T_SEL = (CFG % 27) / 9;
   static constexpr int PIPE_REQ = (CFG / 3) % 3;
   static constexpr int MB = CFG % 3 + 1;
   static constexpr int T = imax(T_SEL ? 512 : 256, P);          // threads per CTA

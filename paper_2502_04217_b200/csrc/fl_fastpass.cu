@@ -387,6 +387,9 @@ Entry make512(int kind, bool epi, int cfg) {
     case cfg_code(1, 2, 1): return make_cfg<512, S, cfg_code(1, 2, 1)>(kind, epi);
     case cfg_code(0, 0, 3): return make_cfg<512, S, cfg_code(0, 0, 3)>(kind, epi);
     case cfg_code(0, 1, 2): return make_cfg<512, S, cfg_code(0, 1, 2)>(kind, epi);
+    case cfg_code(0, 0, 2, 1): return make_cfg<512, S, cfg_code(0, 0, 2, 1)>(kind, epi);
+    case cfg_code(0, 1, 2, 1): return make_cfg<512, S, cfg_code(0, 1, 2, 1)>(kind, epi);
+    case cfg_code(1, 0, 1, 1): return make_cfg<512, S, cfg_code(1, 0, 1, 1)>(kind, epi);
     default: return Entry();
   }
 }

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 fl = pytest.importorskip("paper_2502_04217_b200")
 
-VARIANTS = [10, 5, 7, 12, 15, 2, 4]
+VARIANTS = [10, 5, 7, 12, 15, 2, 4, 28, 31, 36]
 # the last two give every persistent CTA several tiles (exercises the
 # cross-tile cp.async pipelining)
 DIMS = [(512, 4, 8), (4, 6, 512), (16, 512), (512, 2, 64), (2, 512, 16), (512, 128, 64),

@@ -19,7 +19,8 @@ from paper_2502_04217_b200 import _dev, _lib, workloads  # noqa: E402
 
 # cfg_code(t_sel, pipe, mb) = t_sel * 9 + pipe * 3 + mb - 1
 VARIANTS = {10: "512thr/none/2", 5: "256thr/single/3", 7: "256thr/double/2", 12: "512thr/single/1",
-            15: "512thr/double/1", 2: "256thr/none/3", 4: "256thr/single/2"}
+            15: "512thr/double/1", 2: "256thr/none/3", 4: "256thr/single/2",
+            28: "256thr/none/2/E16", 31: "256thr/single/2/E16", 36: "512thr/none/1/E16"}
 
 
 def main():
