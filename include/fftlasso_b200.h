@@ -110,7 +110,10 @@ FL_API int fl_analyze(fl_plan_t plan, const double* x, double* beta, fl_stream_t
 
 /* One per-axis pass: _synthesize_axis (fourier.py:172-183, analysis = 0)
  * or _analyze_axis (fourier.py:186-198, analysis = 1) along ``axis``.
- * Building block of the slab-sharded transform; in may equal out. */
+ * Building block of the slab-sharded transform; in may equal out.
+ * analysis = 2 runs the tile-copy measurement kernel (same tiles and lanes as
+ * the power-of-two pass, FFT removed) used to separate access-pattern cost
+ * from FFT cost (tools/pass_copy_probe.py). */
 FL_API int fl_axis_pass(fl_plan_t plan, int axis, int analysis, const double* in, double* out,
                         fl_stream_t stream);
 

@@ -157,6 +157,30 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
       __syncthreads();
     }
     double2 v[E];
+    if constexpr (KIND == K_COPY) {
+      // measurement kernel: the same tiles, lanes and loop with the FFT removed
+      if (valid) {
+        const double* px = A.in + Q.bx + (int64_t)q * Q.st;
+        const double* py = A.in + Q.by + (int64_t)q * Q.st;
+        double* ox = A.out + Q.bx + (int64_t)q * Q.st;
+        double* oy = A.out + Q.by + (int64_t)q * Q.st;
+        const int64_t rs = (int64_t)P * Q.st;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if (STRIDED) v[r] = *reinterpret_cast<const double2*>(px + r * rs);
+          else v[r] = make_double2(px[r * rs], Q.by >= 0 ? py[r * rs] : 0.0);
+        }
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if (STRIDED) *reinterpret_cast<double2*>(ox + r * rs) = v[r];
+          else {
+            ox[r * rs] = v[r].x;
+            if (Q.by >= 0) oy[r * rs] = v[r].y;
+          }
+        }
+      }
+      continue;
+    }
     if (KIND == K_ANALYZE) {
       if (PIPE > 0) {
 #pragma unroll
@@ -349,6 +373,7 @@ Entry make_cfg(int kind, bool epi) {
   Entry e;
   using G = Geom<M, CFG>;
   switch (kind) {
+    case K_COPY: e.fn = fast_pass<M, S, K_COPY, false, CFG>; break;
     case K_SYNTH: e.fn = fast_pass<M, S, K_SYNTH, false, CFG>; break;
     case K_ANALYZE:
       e.fn = epi ? fast_pass<M, S, K_ANALYZE, true, CFG> : fast_pass<M, S, K_ANALYZE, false, CFG>;
@@ -401,7 +426,7 @@ int env_cfg(const char* name) {
 
 template <int M, bool S>
 Entry make(int kind, bool epi) {
-  const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE);
+  const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE || kind == K_COPY);
   if constexpr (M == 512) {
     const int over_s = env_cfg("FL_CFG_STRIDED"), over_c = env_cfg("FL_CFG_CONTIG");
     const int over = light ? over_s : over_c;

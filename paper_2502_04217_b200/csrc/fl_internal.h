@@ -30,7 +30,7 @@ struct fl_plan {
 
 namespace fl {
 
-enum PassKind : int { K_SYNTH = 0, K_ANALYZE = 1, K_GRAM = 2, K_RESID = 3 };
+enum PassKind : int { K_SYNTH = 0, K_ANALYZE = 1, K_GRAM = 2, K_RESID = 3, K_COPY = 4 };
 
 struct KktEpi {
   const double* pb = nullptr;   // d_beta

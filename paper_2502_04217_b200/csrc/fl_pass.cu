@@ -283,6 +283,7 @@ int run_pass_n(const fl_plan* p, int axis, int kind, const double* in, double* o
   }();
   if (!force_generic && fast_supported(A.m))
     return launch_fast(A.m, strided, kind, epi != nullptr, A, nblocks, s);
+  if (kind == K_COPY) return fail(FL_E_VALUE, "tile-copy probe needs a power-of-two axis <= 8192");
   A.fs = A.m + 1;
   const int per_fibre = 2 * A.fs * (int)sizeof(double2);
   if (per_fibre > 226 * 1024)

@@ -221,8 +221,9 @@ int fl_analyze(fl_plan_t p, const double* x, double* beta, fl_stream_t stream) {
 int fl_axis_pass(fl_plan_t p, int axis, int analysis, const double* in, double* out, fl_stream_t stream) {
   if (!p || !in || !out) return fail(FL_E_VALUE, "null argument");
   if (axis < 0 || axis >= p->ndim) return fail(FL_E_VALUE, "axis out of range");
-  return run_pass(p, axis, analysis ? K_ANALYZE : K_SYNTH, in, out, nullptr, nullptr, nullptr, nullptr,
-                  (cudaStream_t)stream);
+  // analysis == 2: tile-copy measurement kernel (same tiles/lanes, no FFT; power-of-two axes)
+  const int kind = analysis == 2 ? K_COPY : (analysis ? K_ANALYZE : K_SYNTH);
+  return run_pass(p, axis, kind, in, out, nullptr, nullptr, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 int fl_fused_mask_pass(fl_plan_t p, const uint32_t* bits, const double* bhat, const double* in, double* out,
