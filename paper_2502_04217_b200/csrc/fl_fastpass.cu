@@ -20,6 +20,7 @@
 
 #include "fl_common.cuh"
 #include "fl_fast.cuh"
+#include "fl_mirror.cuh"
 #include "fl_internal.h"
 #include "fl_passargs.cuh"
 
@@ -363,6 +364,173 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
   }
 }
 
+// ---------------------------------------------------------------------------
+// Mirrored-butterfly passes (fl_mirror.cuh) for M = 8^k: the pack and unpack
+// read the mirror partner from the thread's own registers, so a pass needs only
+// the NST-1 inter-stage shared-memory exchanges.
+// ---------------------------------------------------------------------------
+template <int M, bool STRIDED, int KIND, bool EPI, int PIPE>
+__global__ void __launch_bounds__(mirror::MGeom<M>::T, 2) mirror_pass(const PassArgs A) {
+  using G = mirror::MGeom<M>;
+  constexpr int CFG = cfg_code(0, PIPE, 2, 1);  // staging geometry shared with Geom<M, CFG>
+  static_assert(Geom<M, CFG>::P == G::P && Geom<M, CFG>::W == G::W, "staging geometry mismatch");
+  static_assert(Geom<M, CFG>::PIPE == PIPE, "staging does not fit");
+  constexpr int P = G::P, W = G::W, H = G::H;
+  extern __shared__ double2 smem[];
+  __shared__ double red[32];
+  int c, q;
+  lane_map<STRIDED>(threadIdx.x, W, P, c, q);
+  const bool q0 = q == 0;
+  double2* fib = smem + c * G::FS;
+  double2* stage0 = smem + G::FIB_BYTES / 16;
+  const double2* tw = A.plan.tw;
+  const double c0 = A.c0, c1 = A.c1;
+  double acc = 0.0, nrm = 0.0;
+  const int64_t ntiles = (A.G + W - 1) / W;
+  if (PIPE > 0) {
+    if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, CFG>(A, blockIdx.x, stage0, c, q);
+    cp_commit();
+  }
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t g = tile * W + c;
+    const bool valid = g < A.G;
+    const Geo Q = geo<STRIDED>(A, valid ? g : 0);
+    const int64_t next = tile + gridDim.x;
+    if (PIPE > 0) {
+      cp_wait<0>();
+      __syncthreads();
+    }
+    double2 v[16];
+    if (KIND == K_ANALYZE) {
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          v[8 * b + s] = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, mirror::slot_k<M>(q, b, s), c);
+    } else {
+      // Zin_k from the packed rows of j = min(k, M - k)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const int k = mirror::slot_k<M>(q, b, s);
+          double2 z;
+          if (k == 0 || k == H) {
+            const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, k == 0 ? 0 : 1, c);
+            z = make_double2(c0 * a.x, c0 * a.y);
+          } else if (k < H) {
+            const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, k + 1, c);
+            const double2 bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, k + H, c);
+            z = make_double2(c1 * (a.x - bb.y), c1 * (bb.x + a.y));
+          } else {
+            const int j = M - k;
+            const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + 1, c);
+            const double2 bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + H, c);
+            z = make_double2(c1 * (a.x + bb.y), c1 * (a.y - bb.x));
+          }
+          v[8 * b + s] = z;
+        }
+    }
+    refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
+    if (KIND == K_ANALYZE) {
+      mirror::fft<M>(v, fib, q, tw, -1);
+    } else {
+      mirror::fft<M>(v, fib, q, tw, +1);
+      if (KIND == K_SYNTH) {
+        if (valid) {
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              const int64_t t = mirror::slot_k<M>(q, b, s);
+              if (STRIDED) *reinterpret_cast<double2*>(A.out + Q.bx + t * Q.st) = v[8 * b + s];
+              else {
+                A.out[Q.bx + t] = v[8 * b + s].x;
+                if (Q.by >= 0) A.out[Q.by + t] = v[8 * b + s].y;
+              }
+            }
+        }
+      } else {
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            double2 z = v[8 * b + s];
+            if (valid) {
+              const int64_t t = mirror::slot_k<M>(q, b, s);
+              const int64_t vx = Q.bx + t * Q.st;
+              const bool mx = missing(A.bits, vx);
+              if (KIND == K_RESID) z.x = mx ? 0.0 : A.bhat[vx] - z.x;
+              else if (mx) z.x = 0.0;
+              if (Q.by >= 0) {
+                const int64_t vy = Q.by + t * Q.st;
+                const bool my = missing(A.bits, vy);
+                if (KIND == K_RESID) z.y = my ? 0.0 : A.bhat[vy] - z.y;
+                else if (my) z.y = 0.0;
+              } else {
+                z.y = 0.0;
+              }
+              if (KIND == K_GRAM) nrm += z.x * z.x + z.y * z.y;
+            }
+            v[8 * b + s] = z;
+          }
+        mirror::fft<M>(v, fib, q, tw, -1);
+      }
+    }
+    if (KIND != K_SYNTH && valid) {
+      // pack (Z_k, Z_{M-k}) straight from registers for the 8 slots with k < H
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const int j = mirror::slot_k<M>(q, b, s);
+          const double2 a = v[8 * b + s];
+          double xa, xb, ya, yb;
+          int64_t ia, ib;
+          if (b == 0 && s == 0 && q0) {
+            const double2 zh = v[4];  // Z_H of q = 0
+            xa = c0 * a.x; ya = c0 * a.y;
+            xb = c0 * zh.x; yb = c0 * zh.y;
+            ia = 0;
+            ib = Q.st;
+          } else {
+            // mirror partner of slot (b, s) (indices are constants after unrolling)
+            const double2 m = q0 ? v[8 * b + (b == 0 ? ((8 - s) & 7) : (7 - s))] : v[8 * (1 - b) + 7 - s];
+            xa = c1 * (a.x + m.x);
+            xb = c1 * (a.y - m.y);
+            ya = c1 * (a.y + m.y);
+            yb = c1 * (m.x - a.x);
+            ia = Q.st * (j + 1);
+            ib = Q.st * (j + H);
+          }
+          if (STRIDED && !EPI) {
+            *reinterpret_cast<double2*>(A.out + Q.bx + ia) = make_double2(xa, ya);
+            *reinterpret_cast<double2*>(A.out + Q.bx + ib) = make_double2(xb, yb);
+          } else if (STRIDED) {
+            kkt_store2(A, Q.bx + ia, xa, ya, acc);
+            kkt_store2(A, Q.bx + ib, xb, yb, acc);
+          } else {
+            put<STRIDED, EPI>(A, Q.bx + ia, xa, acc);
+            put<STRIDED, EPI>(A, Q.bx + ib, xb, acc);
+            if (Q.by >= 0) {
+              put<STRIDED, EPI>(A, Q.by + ia, ya, acc);
+              put<STRIDED, EPI>(A, Q.by + ib, yb, acc);
+            }
+          }
+        }
+    }
+  }
+  if (PIPE > 0) cp_wait<0>();
+  if (EPI && A.epi.partials) {
+    const double s = block_reduce(acc, SumOp(), red);
+    if (threadIdx.x == 0) A.epi.partials[blockIdx.x] = s;
+  }
+  if (KIND == K_GRAM && A.nrm_partials) {
+    const double s = block_reduce(nrm, SumOp(), red);
+    if (threadIdx.x == 0) A.nrm_partials[blockIdx.x] = s;
+  }
+}
+
 struct Entry {
   KernelFn fn = nullptr;
   int threads = 0, smem = 0, w = 0;
@@ -424,9 +592,49 @@ int env_cfg(const char* name) {
   return v ? std::atoi(v) : -1;
 }
 
+template <int M, bool S, int PIPE>
+Entry make_mirror(int kind, bool epi) {
+  Entry e;
+  using G = mirror::MGeom<M>;
+  switch (kind) {
+    case K_SYNTH: e.fn = mirror_pass<M, S, K_SYNTH, false, PIPE>; break;
+    case K_ANALYZE:
+      e.fn = epi ? mirror_pass<M, S, K_ANALYZE, true, PIPE> : mirror_pass<M, S, K_ANALYZE, false, PIPE>;
+      break;
+    case K_GRAM:
+      if constexpr (!S)
+        e.fn = epi ? mirror_pass<M, false, K_GRAM, true, PIPE> : mirror_pass<M, false, K_GRAM, false, PIPE>;
+      break;
+    case K_RESID:
+      if constexpr (!S)
+        e.fn = epi ? mirror_pass<M, false, K_RESID, true, PIPE> : mirror_pass<M, false, K_RESID, false, PIPE>;
+      break;
+    default: break;
+  }
+  e.threads = G::T;
+  e.smem = G::FIB_BYTES + PIPE * G::STAGE_BYTES;
+  e.w = G::W;
+  return e;
+}
+
+// FL_MIRROR: 0 off, 1 staging per kind (light passes direct, others single
+// cp.async buffer), 2 no staging, 3 single staging for every kind.
+int mirror_mode() {
+  const char* v = std::getenv("FL_MIRROR");
+  return v ? std::atoi(v) : 0;
+}
+
 template <int M, bool S>
 Entry make(int kind, bool epi) {
   const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE || kind == K_COPY);
+  if constexpr (M == 64 || M == 512 || M == 4096) {
+    const int mm = kind == K_COPY ? 0 : mirror_mode();
+    if (mm > 0) {
+      const bool pipe = mm == 3 || (mm == 1 && !light);
+      Entry e = pipe ? make_mirror<M, S, 1>(kind, epi) : make_mirror<M, S, 0>(kind, epi);
+      if (e.fn) return e;
+    }
+  }
   if constexpr (M == 512) {
     const int over_s = env_cfg("FL_CFG_STRIDED"), over_c = env_cfg("FL_CFG_CONTIG");
     const int over = light ? over_s : over_c;

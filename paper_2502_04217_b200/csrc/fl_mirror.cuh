@@ -1,0 +1,112 @@
+// "Mirrored" register FFT engine for M = 8^k (64, 512, 4096), sm_100a.
+//
+// Every stage is radix 8 with NB = M/8 butterflies per fibre; a fibre is owned
+// by P = NB/2 threads and thread q owns the two MIRRORED butterflies
+//
+//     b = 0 : qq = q              b = 1 : qq = NB - q   (q = 0: qq = NB/2)
+//
+// Butterfly qq reads positions qq + s*NB and, in the last stage, writes
+// qq + s*NB, so slot (b, s) of thread q holds index k = qq_b + s*NB and its
+// mirror M - k sits in the SAME thread:
+//
+//     q != 0 : (b, s) <-> (1 - b, 7 - s)
+//     q == 0 : (0, s) <-> (0, (8 - s) mod 8),  (1, s) <-> (1, 7 - s)
+//
+// so the real-pair pack (Z_k, Z_{M-k}) and the unpack (Zin_k from the packed
+// rows of min(k, M-k)) need no shared-memory exchange; only the NST-1
+// inter-stage exchanges remain.  Registers: v[b*8 + s].
+#pragma once
+
+#include "fl_fast.cuh"
+
+namespace fl {
+namespace mirror {
+
+using fast::si;
+
+constexpr int log8(int m) { return m <= 1 ? 0 : 1 + log8(m / 8); }
+
+template <int M>
+struct MGeom {
+  static constexpr int E = 16;
+  static constexpr int NB = M / 8;                          // butterflies per fibre per stage
+  static constexpr int P = NB / 2;                          // threads per fibre
+  static constexpr int T = fast::imax(256, P);              // threads per CTA
+  static constexpr int W = T / P;                           // fibres per CTA tile
+  static constexpr int NST = log8(M);
+  static constexpr int FS = M + M / 8 + 1;                  // smem fibre stride (double2)
+  static constexpr int FIB_BYTES = W * FS * 16;
+  static constexpr int STAGE_BYTES = W * M * 16;
+  static constexpr int H = M / 2;
+  static constexpr int ns(int s) { return s == 0 ? 1 : 8 * ns(s - 1); }
+};
+
+__device__ __forceinline__ int own(int q, int b, int nb) { return b == 0 ? q : (q == 0 ? nb / 2 : nb - q); }
+
+// One radix-8 stage on both butterflies (twiddles from the length-M table).
+template <int M, int S>
+__device__ __forceinline__ void stage(double2* v, int q, const double2* tw, int sign) {
+  using G = MGeom<M>;
+  constexpr int NS = G::ns(S);
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    double2* u = v + 8 * b;
+    if constexpr (NS > 1) {
+      const int qq = own(q, b, G::NB);
+      const int j = qq % NS;
+      double2 w[8];
+      fast::twiddles<M, 8, NS>(w, j, tw, sign);
+#pragma unroll
+      for (int s = 1; s < 8; ++s) u[s] = cmul(u[s], w[s]);
+    }
+    dft8(u, sign);
+  }
+}
+
+// Exchange after stage S: outputs to their Stockham destinations, then the
+// inputs of stage S+1 (positions qq + s*NB of the thread's butterflies).
+template <int M, int S>
+__device__ __forceinline__ void exchange(double2* v, double2* fib, int q) {
+  using G = MGeom<M>;
+  constexpr int NS = G::ns(S), NB = G::NB;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const int qq = own(q, b, NB);
+    if constexpr (NS == 1) {
+      double2* o = fib + 9 * qq;  // si(8 qq + s) = 9 qq + s
+#pragma unroll
+      for (int s = 0; s < 8; ++s) o[s] = v[8 * b + s];
+    } else {
+      const int j = qq % NS;
+      double2* o = fib + si((qq - j) * 8 + j);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) o[s * (NS + NS / 8)] = v[8 * b + s];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const double2* o = fib + si(own(q, b, NB));
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[8 * b + s] = o[s * (NB + NB / 8)];
+  }
+  __syncthreads();
+}
+
+template <int M, int S = 0>
+__device__ __forceinline__ void fft(double2* v, double2* fib, int q, const double2* tw, int sign) {
+  stage<M, S>(v, q, tw, sign);
+  if constexpr (S + 1 < MGeom<M>::NST) {
+    exchange<M, S>(v, fib, q);
+    fft<M, S + 1>(v, fib, q, tw, sign);
+  }
+}
+
+// Index k held by slot (b, s) of thread q.
+template <int M>
+__device__ __forceinline__ int slot_k(int q, int b, int s) {
+  return own(q, b, MGeom<M>::NB) + s * MGeom<M>::NB;
+}
+
+}  // namespace mirror
+}  // namespace fl

@@ -15,7 +15,10 @@ for line in out.splitlines():
     if m:
         cur = m.group(1)
         d = re.search(r"fast_passILi(\d+)ELb(\d)ELi(\d)ELb(\d)ELi(\d+)E", cur)
-        if d:
+        mm = re.search(r"mirror_passILi(\d+)ELb(\d)ELi(\d)ELb(\d)ELi(\d+)E", cur)
+        if mm:
+            cur = f"mirror_pass<M={mm.group(1)},s={mm.group(2)},kind={mm.group(3)},epi={mm.group(4)},pipe={mm.group(5)}>"
+        elif d:
             cur = f"fast_pass<M={d.group(1)},s={d.group(2)},kind={d.group(3)},epi={d.group(4)},cfg={d.group(5)}>"
         else:
             cur = re.sub(r"_ZN2fl\d+_GLOBAL__N__\w+?_\d+(\w+?)E.*", r"\1", cur)[:60]

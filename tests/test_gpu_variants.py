@@ -37,18 +37,38 @@ def _mask(dims, rng):
 @pytest.mark.parametrize("which", ["FL_CFG_STRIDED", "FL_CFG_CONTIG"])
 def test_variant_matches_oracle(var, which, monkeypatch):
     monkeypatch.setenv(which, str(var))
-    rng = np.random.default_rng(var)
+    _check_all_dims(var)
+
+
+@pytest.mark.parametrize("mode", ["1", "2", "3"])
+def test_mirror_engine_matches_oracle(mode, monkeypatch):
+    """The mirrored-butterfly engine (FL_MIRROR, m = 64 / 512 / 4096)."""
+    monkeypatch.setenv("FL_MIRROR", mode)
+    _check_all_dims(int(mode) + 100)
+    for dims in [(64, 8, 16), (4096,), (8, 4096), (64, 64, 64), (4096, 4)]:
+        _check_dims(dims, np.random.default_rng(len(dims)))
+
+
+def _check_all_dims(seed):
+    rng = np.random.default_rng(seed)
     for dims in DIMS:
-        shape = fl.GridShape(dims)
-        flags = _mask(dims, rng)
-        mask = fl.Mask.from_bool(flags, shape)
-        om = orc.make_mask(dims, flags=flags)
-        beta = rng.standard_normal(shape.n)
-        x = rng.standard_normal(shape.n)
-        tol = 1e-12 * max(1.0, np.abs(beta).max())
-        assert np.max(np.abs(fl.synthesize(beta, shape) - orc.synthesize(beta, dims))) <= tol, dims
-        assert np.max(np.abs(fl.analyze(x, shape) - orc.analyze(x, dims))) <= tol, dims
-        assert np.max(np.abs(fl.gram(beta, mask) - orc.gram(beta, om))) <= tol, dims
+        _check_dims(dims, rng)
+
+
+def _check_dims(dims, rng):
+    shape = fl.GridShape(dims)
+    flags = _mask(dims, rng)
+    mask = fl.Mask.from_bool(flags, shape)
+    om = orc.make_mask(dims, flags=flags)
+    beta = rng.standard_normal(shape.n)
+    x = rng.standard_normal(shape.n)
+    tol = 1e-12 * max(1.0, np.abs(beta).max())
+    assert np.max(np.abs(fl.synthesize(beta, shape) - orc.synthesize(beta, dims))) <= tol, dims
+    assert np.max(np.abs(fl.analyze(x, shape) - orc.analyze(x, dims))) <= tol, dims
+    assert np.max(np.abs(fl.gram(beta, mask) - orc.gram(beta, om))) <= tol, dims
+    w = rng.standard_normal(mask.n_observed)
+    ref = orc.observe_adjoint(w, om)
+    assert np.max(np.abs(fl.observe_adjoint(w, mask) - ref)) <= 1e-12 * max(1.0, np.abs(ref).max()), dims
 
 
 def test_generic_engine_matches_oracle():

@@ -69,6 +69,14 @@ def main():
             print(f"{which}={cfg:2d} {name:18s} passes_ms={np.round(ms, 4).tolist()} total={ms.sum():.4f} "
                   f"maxdiff={err:.1e}", flush=True)
         del os.environ[which]
+    for mm in ("1", "2", "3"):
+        os.environ["FL_MIRROR"] = mm
+        ms = run()
+        err = float((top - ref).abs().max())
+        results[f"FL_MIRROR={mm}"] = [round(x, 4) for x in ms]
+        print(f"FL_MIRROR={mm} passes_ms={np.round(ms, 4).tolist()} total={ms.sum():.4f} maxdiff={err:.1e}",
+              flush=True)
+    del os.environ["FL_MIRROR"]
     print(json.dumps(results))
 
 
