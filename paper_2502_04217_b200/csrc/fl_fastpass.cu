@@ -408,28 +408,54 @@ __global__ void __launch_bounds__(mirror::MGeom<M>::T, 2) mirror_pass(const Pass
         for (int s = 0; s < 8; ++s)
           v[8 * b + s] = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, mirror::slot_k<M>(q, b, s), c);
     } else {
-      // Zin_k from the packed rows of j = min(k, M - k)
-#pragma unroll
-      for (int b = 0; b < 2; ++b)
+      // Zin_j and Zin_{M-j} from ONE read of the packed rows (j+1, j+H) of
+      // j = min(k, M-k); the two values land in the mirror slot pair.
+      auto rows = [&](int j, double2& a, double2& bb) {
+        a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + 1, c);
+        bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + H, c);
+      };
+      auto lo = [&](const double2& a, const double2& bb) {  // Zin_j
+        return make_double2(c1 * (a.x - bb.y), c1 * (bb.x + a.y));
+      };
+      auto hi = [&](const double2& a, const double2& bb) {  // Zin_{M-j}
+        return make_double2(c1 * (a.x + bb.y), c1 * (a.y - bb.x));
+      };
+      if (!q0) {
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
-          const int k = mirror::slot_k<M>(q, b, s);
-          double2 z;
-          if (k == 0 || k == H) {
-            const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, k == 0 ? 0 : 1, c);
-            z = make_double2(c0 * a.x, c0 * a.y);
-          } else if (k < H) {
-            const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, k + 1, c);
-            const double2 bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, k + H, c);
-            z = make_double2(c1 * (a.x - bb.y), c1 * (bb.x + a.y));
+          // pair: slot (0, s) holds k0 = q + s NB, slot (1, 7-s) holds M - k0
+          const int j = s < 4 ? mirror::slot_k<M>(q, 0, s) : mirror::slot_k<M>(q, 1, 7 - s);
+          double2 a, bb;
+          rows(j, a, bb);
+          if (s < 4) {
+            v[s] = lo(a, bb);
+            v[8 + 7 - s] = hi(a, bb);
           } else {
-            const int j = M - k;
-            const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + 1, c);
-            const double2 bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + H, c);
-            z = make_double2(c1 * (a.x + bb.y), c1 * (a.y - bb.x));
+            v[8 + 7 - s] = lo(a, bb);
+            v[s] = hi(a, bb);
           }
-          v[8 * b + s] = z;
         }
+      } else {
+        // q == 0: butterflies 0 and NB/2 are self-mirrored
+        const double2 r0 = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 0, c);
+        const double2 r1 = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 1, c);
+        v[0] = make_double2(c0 * r0.x, c0 * r0.y);
+        v[4] = make_double2(c0 * r1.x, c0 * r1.y);
+#pragma unroll
+        for (int s = 1; s < 4; ++s) {
+          double2 a, bb;
+          rows(mirror::slot_k<M>(0, 0, s), a, bb);
+          v[s] = lo(a, bb);
+          v[8 - s] = hi(a, bb);
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          double2 a, bb;
+          rows(mirror::slot_k<M>(0, 1, s), a, bb);
+          v[8 + s] = lo(a, bb);
+          v[8 + 7 - s] = hi(a, bb);
+        }
+      }
     }
     refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
     if (KIND == K_ANALYZE) {
@@ -618,17 +644,20 @@ Entry make_mirror(int kind, bool epi) {
 }
 
 // FL_MIRROR: 0 off, 1 staging per kind (light passes direct, others single
-// cp.async buffer), 2 no staging, 3 single staging for every kind.
+// cp.async buffer), 2 no staging, 3 single staging for every kind,
+// 4 (default) plain strided synthesis/analysis only, no staging -- the
+// measured best (tools/sweep_cfg.py); the fused gram pass keeps the E=8 engine.
 int mirror_mode() {
   const char* v = std::getenv("FL_MIRROR");
-  return v ? std::atoi(v) : 0;
+  return v ? std::atoi(v) : 4;
 }
 
 template <int M, bool S>
 Entry make(int kind, bool epi) {
   const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE || kind == K_COPY);
   if constexpr (M == 64 || M == 512 || M == 4096) {
-    const int mm = kind == K_COPY ? 0 : mirror_mode();
+    int mm = kind == K_COPY ? 0 : mirror_mode();
+    if (mm == 4) mm = light ? 2 : 0;
     if (mm > 0) {
       const bool pipe = mm == 3 || (mm == 1 && !light);
       Entry e = pipe ? make_mirror<M, S, 1>(kind, epi) : make_mirror<M, S, 0>(kind, epi);
