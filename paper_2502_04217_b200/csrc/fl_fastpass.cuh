@@ -1,0 +1,707 @@
+// Register-resident axis passes (kernel templates; instantiated per length in fl_fp_*.cu) for power-of-two fibre lengths 16..8192
+// (the hot path at every BASELINE size).  Same data model and fusion as the
+// generic passes in fl_pass.cu (paired fibres, pack/unpack + ortho scale in
+// the load/store stages, one fused last-axis synth+mask+analysis pass, KKT
+// epilogue in the final store), with the FFT held in registers:
+//
+//   synthesis   global rows (j+1, j+h) -> unpack -> smem -> registers ->
+//               inverse FFT (NST-1 smem exchanges) -> registers -> global
+//   analysis    global -> registers -> forward FFT -> smem -> pack -> global
+//   gram/resid  unpack -> inverse FFT -> mask (in registers) -> forward FFT
+//               (consumes the inverse FFT's register layout directly) -> pack
+//
+// A persistent grid (resident CTAs x 148 SMs) walks the tiles.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+#include <string>
+
+#include "fl_common.cuh"
+#include "fl_fast.cuh"
+#include "fl_mirror.cuh"
+#include "fl_internal.h"
+#include "fl_passargs.cuh"
+
+namespace fl {
+namespace fpk {
+
+using fast::Geom;
+using fast::si;
+using fast::cfg_code;
+using fast::cp_async16;
+using fast::cp_async8;
+using fast::cp_commit;
+using fast::cp_wait;
+
+template <bool STRIDED>
+__device__ __forceinline__ void lane_map(int tid, int W, int P, int& c, int& q) {
+  if (STRIDED) { c = tid % W; q = tid / W; }  // fibre-fast: 128-byte row segments per quarter-warp
+  else { q = tid % P; c = tid / P; }          // position-fast: contiguous rows
+}
+
+// 16-byte KKT epilogue for a strided-axis pair (x at v, y at v + 1).
+__device__ __forceinline__ void kkt_store2(const PassArgs& A, int64_t v, double gx, double gy,
+                                           double& acc) {
+  const double2 pb = *reinterpret_cast<const double2*>(A.epi.pb + v);
+  const double2 pz = *reinterpret_cast<const double2*>(A.epi.pz + v);
+  const double2 s1 = *reinterpret_cast<const double2*>(A.epi.sig1 + v);
+  const double2 s2 = *reinterpret_cast<const double2*>(A.epi.sig2 + v);
+  double2 top, bot;
+  {
+    const double l1 = add(s1.x, s2.x), l2 = sub(s1.x, s2.x);
+    top.x = add(add(gx, mul(l1, pb.x)), mul(l2, pz.x));
+    bot.x = add(mul(l2, pb.x), mul(l1, pz.x));
+  }
+  {
+    const double l1 = add(s1.y, s2.y), l2 = sub(s1.y, s2.y);
+    top.y = add(add(gy, mul(l1, pb.y)), mul(l2, pz.y));
+    bot.y = add(mul(l2, pb.y), mul(l1, pz.y));
+  }
+  *reinterpret_cast<double2*>(A.out + v) = top;
+  if (A.epi.bottom) *reinterpret_cast<double2*>(A.epi.bottom + v) = bot;
+  acc += pb.x * top.x + pz.x * bot.x + pb.y * top.y + pz.y * bot.y;
+}
+
+// Raw input tile staging: element (k, fibre c) of the tile.
+template <int M, bool STRIDED, int CFG>
+__device__ __forceinline__ int stage_idx(int k, int c) {
+  return STRIDED ? k * Geom<M, CFG>::W + c : c * M + k;
+}
+
+// Issue this thread's cp.async copies of tile ``tile`` (its natural-layout
+// elements k = q + r P of fibre c) into ``st``.
+template <int M, bool STRIDED, int CFG>
+__device__ __forceinline__ void issue_tile(const PassArgs& A, int64_t tile, double2* st, int c, int q) {
+  using G = Geom<M, CFG>;
+  const int64_t g = tile * G::W + c;
+  if (g >= A.G) return;
+  const Geo Q = geo<STRIDED>(A, g);
+#pragma unroll
+  for (int r = 0; r < G::E; ++r) {
+    const int k = q + r * G::P;
+    double2* dst = st + stage_idx<M, STRIDED, CFG>(k, c);
+    if (STRIDED) {
+      cp_async16(dst, A.in + Q.bx + k * Q.st);
+    } else {
+      cp_async8(&dst->x, A.in + Q.bx + k);
+      if (Q.by >= 0) cp_async8(&dst->y, A.in + Q.by + k);
+    }
+  }
+}
+
+// Element (k, c) of the current raw tile: from staging (pipelined) or global.
+template <int M, bool STRIDED, bool PIPE, int CFG>
+__device__ __forceinline__ double2 raw(const PassArgs& A, const double2* st, const Geo& Q, bool valid,
+                                       int k, int c) {
+  double2 z = make_double2(0.0, 0.0);
+  if (!valid) return z;
+  if (PIPE) {
+    z = st[stage_idx<M, STRIDED, CFG>(k, c)];
+    if (!STRIDED && Q.by < 0) z.y = 0.0;
+  } else if (STRIDED) {
+    z = *reinterpret_cast<const double2*>(A.in + Q.bx + (int64_t)k * Q.st);
+  } else {
+    z.x = A.in[Q.bx + k];
+    if (Q.by >= 0) z.y = A.in[Q.by + k];
+  }
+  return z;
+}
+
+// Single-buffer staging: once every thread has read the current tile out of
+// the stage, start copying the next tile into it (overlaps this tile's FFT).
+template <int M, bool STRIDED, int CFG>
+__device__ __forceinline__ void refill(const PassArgs& A, int64_t next, int64_t ntiles, double2* stage,
+                                       int c, int q) {
+  if constexpr (Geom<M, CFG>::PIPE == 1) {
+    __syncthreads();
+    if (next < ntiles) issue_tile<M, STRIDED, CFG>(A, next, stage, c, q);
+    cp_commit();
+  }
+}
+
+template <int M, bool STRIDED, int KIND, bool EPI, int CFG>
+__global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(const PassArgs A) {
+  using G = Geom<M, CFG>;
+  constexpr int E = G::E, P = G::P, W = G::W, H = M / 2;
+  constexpr int PIPE = G::PIPE;  // 0 none, 1 single, 2 double buffered staging
+  extern __shared__ double2 smem[];
+  __shared__ double red[32];
+  int c, q;
+  lane_map<STRIDED>(threadIdx.x, W, P, c, q);
+  double2* fib = smem + c * G::FS;
+  double2* stage0 = smem + G::FIB_BYTES / 16;
+  double2* stage1 = stage0 + W * M;
+  const double2* tw = A.plan.tw;
+  const double c0 = A.c0, c1 = A.c1;
+  double acc = 0.0, nrm = 0.0;
+  const int64_t ntiles = (A.G + W - 1) / W;
+  if (PIPE > 0) {
+    if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, CFG>(A, blockIdx.x, stage0, c, q);
+    cp_commit();
+  }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int64_t g = tile * W + c;
+    const bool valid = g < A.G;
+    const Geo Q = geo<STRIDED>(A, valid ? g : 0);
+    const int64_t next = tile + gridDim.x;
+    const double2* st = (PIPE == 2 && (it & 1)) ? stage1 : stage0;
+    if (PIPE == 2) {
+      if (next < ntiles) issue_tile<M, STRIDED, CFG>(A, next, (it & 1) ? stage0 : stage1, c, q);
+      cp_commit();
+      cp_wait<1>();
+      __syncthreads();
+    } else if (PIPE == 1) {
+      cp_wait<0>();
+      __syncthreads();
+    }
+    double2 v[E];
+    if constexpr (KIND == K_COPY) {
+      // measurement kernel: the same tiles, lanes and loop with the FFT removed
+      if (valid) {
+        const double* px = A.in + Q.bx + (int64_t)q * Q.st;
+        const double* py = A.in + Q.by + (int64_t)q * Q.st;
+        double* ox = A.out + Q.bx + (int64_t)q * Q.st;
+        double* oy = A.out + Q.by + (int64_t)q * Q.st;
+        const int64_t rs = (int64_t)P * Q.st;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if (STRIDED) v[r] = *reinterpret_cast<const double2*>(px + r * rs);
+          else v[r] = make_double2(px[r * rs], Q.by >= 0 ? py[r * rs] : 0.0);
+        }
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if (STRIDED) *reinterpret_cast<double2*>(ox + r * rs) = v[r];
+          else {
+            ox[r * rs] = v[r].x;
+            if (Q.by >= 0) oy[r * rs] = v[r].y;
+          }
+        }
+      }
+      continue;
+    }
+    if (KIND == K_ANALYZE) {
+      if (PIPE > 0) {
+#pragma unroll
+        for (int r = 0; r < E; ++r) v[r] = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, q + r * P, c);
+        refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
+      } else {
+        // base pointer of row q, rows advance by P*st (no per-element 64-bit multiplies)
+        const double* px = A.in + Q.bx + (int64_t)q * Q.st;
+        const double* py = A.in + Q.by + (int64_t)q * Q.st;
+        const int64_t rs = (int64_t)P * Q.st;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          double2 z = make_double2(0.0, 0.0);
+          if (valid) {
+            if (STRIDED) z = *reinterpret_cast<const double2*>(px + r * rs);
+            else {
+              z.x = px[r * rs];
+              if (Q.by >= 0) z.y = py[r * rs];
+            }
+          }
+          v[r] = z;
+        }
+      }
+      fast::fft<M, CFG>(v, fib, q, tw, -1);
+    } else {
+      if constexpr (PIPE > 0) {
+        // unpack straight from the staged raw rows into the natural layout:
+        // Zin_k needs rows (k+1, k+h) for k < h and rows (M-k+1, M-k+h) above h
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int k = q + r * P;
+          double2 z;
+          if (r < E / 2) {
+            if (r == 0 && q == 0) {
+              const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, 0, c);
+              z = make_double2(c0 * a.x, c0 * a.y);
+            } else {
+              const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, k + 1, c);
+              const double2 b = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, k + H, c);
+              z = make_double2(c1 * (a.x - b.y), c1 * (b.x + a.y));
+            }
+          } else {
+            if (r == E / 2 && q == 0) {
+              const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, 1, c);
+              z = make_double2(c0 * a.x, c0 * a.y);
+            } else {
+              const int j = M - k;
+              const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, j + 1, c);
+              const double2 b = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, j + H, c);
+              z = make_double2(c1 * (a.x + b.y), c1 * (a.y - b.x));
+            }
+          }
+          v[r] = z;
+        }
+        refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
+      } else {
+        // unpack packed rows (j+1, j+h) into the combined half spectra Zin_j, Zin_{M-j}
+        const int qm = -q + ((-q) >> 3);
+  #pragma unroll
+        for (int r = 0; r < E / 2; ++r) {
+          const int j = q + r * P;
+          const bool j0 = r == 0 && q == 0;
+          const double2 a = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, j0 ? 0 : j + 1, c);
+          const double2 b = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, j0 ? 1 : j + H, c);
+          const double xa = a.x, ya = a.y, xb = b.x, yb = b.y;
+          if (j0) {
+            fib[0] = make_double2(c0 * xa, c0 * ya);
+            fib[si(H)] = make_double2(c0 * xb, c0 * yb);
+          } else {
+            fib[fast::lo_idx<M, CFG>(q, r)] = make_double2(c1 * (xa - yb), c1 * (xb + ya));
+            fib[fast::hi_idx<M, CFG>(q, qm, r)] = make_double2(c1 * (xa + yb), c1 * (ya - xb));
+          }
+        }
+        __syncthreads();
+        fast::load_natural<M, CFG>(v, fib, q);
+        __syncthreads();
+      }
+      // mask words for this thread's samples, fetched before the inverse FFT so
+      // their latency hides behind it (one 32-bit word per sample, L1/L2 hits)
+      uint32_t wx[(KIND == K_GRAM || KIND == K_RESID) ? E : 1];
+      uint32_t wy[(KIND == K_GRAM || KIND == K_RESID) ? E : 1];
+      if constexpr (KIND == K_GRAM || KIND == K_RESID) {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int64_t vx = Q.bx + q + r * P;
+          wx[r] = valid ? __ldg(A.bits + (vx >> 5)) : 0u;
+          wy[r] = (valid && Q.by >= 0) ? __ldg(A.bits + ((Q.by + q + r * P) >> 5)) : 0u;
+        }
+      }
+      fast::fft<M, CFG>(v, fib, q, tw, +1);
+      if (KIND == K_SYNTH) {
+        if (valid) {
+          double* px = A.out + Q.bx + (int64_t)q * Q.st;
+          double* py = A.out + Q.by + (int64_t)q * Q.st;
+          const int64_t rs = (int64_t)P * Q.st;
+#pragma unroll
+          for (int r = 0; r < E; ++r) {
+            if (STRIDED) *reinterpret_cast<double2*>(px + r * rs) = v[r];
+            else {
+              px[r * rs] = v[r].x;
+              if (Q.by >= 0) py[r * rs] = v[r].y;
+            }
+          }
+        }
+      } else {
+        // Z (b_hat - x) or Z x on the synthesized samples, in registers
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int t = q + r * P;
+          double2 z = v[r];
+          if (valid) {
+            const int64_t vx = Q.bx + t;
+            const bool mx = (wx[r] >> (vx & 31)) & 1u;
+            if (KIND == K_RESID) z.x = mx ? 0.0 : A.bhat[vx] - z.x;
+            else if (mx) z.x = 0.0;
+            if (Q.by >= 0) {
+              const int64_t vy = Q.by + t;
+              const bool my = (wy[r] >> (vy & 31)) & 1u;
+              if (KIND == K_RESID) z.y = my ? 0.0 : A.bhat[vy] - z.y;
+              else if (my) z.y = 0.0;
+            } else {
+              z.y = 0.0;
+            }
+            if (KIND == K_GRAM) nrm += z.x * z.x + z.y * z.y;  // ||Z A beta||^2 = beta . G beta
+          }
+          v[r] = z;
+        }
+        fast::fft<M, CFG>(v, fib, q, tw, -1);
+      }
+    }
+    if (KIND != K_SYNTH) {
+      fast::store_natural<M, CFG>(v, fib, q);
+      __syncthreads();
+      if (valid) {
+        const int qm = -q + ((-q) >> 3);
+#pragma unroll
+        for (int r = 0; r < E / 2; ++r) {
+          const int j = q + r * P;
+          const bool j0 = r == 0 && q == 0;
+          double xa, xb, ya, yb;
+          if (j0) {
+            const double2 z0 = fib[0], zh = fib[si(H)];
+            xa = c0 * z0.x; ya = c0 * z0.y;
+            xb = c0 * zh.x; yb = c0 * zh.y;
+          } else {
+            const double2 a = fib[fast::lo_idx<M, CFG>(q, r)], b = fib[fast::hi_idx<M, CFG>(q, qm, r)];
+            xa = c1 * (a.x + b.x);
+            xb = c1 * (a.y - b.y);
+            ya = c1 * (a.y + b.y);
+            yb = c1 * (b.x - a.x);
+          }
+          const int64_t ia = Q.st * (j0 ? 0 : j + 1), ib = Q.st * (j0 ? 1 : j + H);
+          if (STRIDED && !EPI) {
+            *reinterpret_cast<double2*>(A.out + Q.bx + ia) = make_double2(xa, ya);
+            *reinterpret_cast<double2*>(A.out + Q.bx + ib) = make_double2(xb, yb);
+          } else if (STRIDED) {
+            kkt_store2(A, Q.bx + ia, xa, ya, acc);
+            kkt_store2(A, Q.bx + ib, xb, yb, acc);
+          } else {
+            put<STRIDED, EPI>(A, Q.bx + ia, xa, acc);
+            put<STRIDED, EPI>(A, Q.bx + ib, xb, acc);
+            if (Q.by >= 0) {
+              put<STRIDED, EPI>(A, Q.by + ia, ya, acc);
+              put<STRIDED, EPI>(A, Q.by + ib, yb, acc);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (PIPE > 0) cp_wait<0>();
+  if (EPI && A.epi.partials) {
+    const double s = block_reduce(acc, SumOp(), red);
+    if (threadIdx.x == 0) A.epi.partials[blockIdx.x] = s;
+  }
+  if (KIND == K_GRAM && A.nrm_partials) {
+    const double s = block_reduce(nrm, SumOp(), red);
+    if (threadIdx.x == 0) A.nrm_partials[blockIdx.x] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Mirrored-butterfly passes (fl_mirror.cuh) for M = 8^k: the pack and unpack
+// read the mirror partner from the thread's own registers, so a pass needs only
+// the NST-1 inter-stage shared-memory exchanges.
+// ---------------------------------------------------------------------------
+template <int M, bool STRIDED, int KIND, bool EPI, int PIPE>
+__global__ void __launch_bounds__(mirror::MGeom<M>::T, 2) mirror_pass(const PassArgs A) {
+  using G = mirror::MGeom<M>;
+  constexpr int CFG = cfg_code(0, PIPE, 2, 1);  // staging geometry shared with Geom<M, CFG>
+  static_assert(Geom<M, CFG>::P == G::P && Geom<M, CFG>::W == G::W, "staging geometry mismatch");
+  static_assert(Geom<M, CFG>::PIPE == PIPE, "staging does not fit");
+  constexpr int P = G::P, W = G::W, H = G::H;
+  extern __shared__ double2 smem[];
+  __shared__ double red[32];
+  int c, q;
+  lane_map<STRIDED>(threadIdx.x, W, P, c, q);
+  const bool q0 = q == 0;
+  double2* fib = smem + c * G::FS;
+  double2* stage0 = smem + G::FIB_BYTES / 16;
+  const double2* tw = A.plan.tw;
+  const double c0 = A.c0, c1 = A.c1;
+  double acc = 0.0, nrm = 0.0;
+  const int64_t ntiles = (A.G + W - 1) / W;
+  if (PIPE > 0) {
+    if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, CFG>(A, blockIdx.x, stage0, c, q);
+    cp_commit();
+  }
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t g = tile * W + c;
+    const bool valid = g < A.G;
+    const Geo Q = geo<STRIDED>(A, valid ? g : 0);
+    const int64_t next = tile + gridDim.x;
+    if (PIPE > 0) {
+      cp_wait<0>();
+      __syncthreads();
+    }
+    double2 v[16];
+    if (KIND == K_ANALYZE) {
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          v[8 * b + s] = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, mirror::slot_k<M>(q, b, s), c);
+    } else {
+      // Zin_j and Zin_{M-j} from ONE read of the packed rows (j+1, j+H) of
+      // j = min(k, M-k); the two values land in the mirror slot pair.
+      auto rows = [&](int j, double2& a, double2& bb) {
+        a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + 1, c);
+        bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + H, c);
+      };
+      auto lo = [&](const double2& a, const double2& bb) {  // Zin_j
+        return make_double2(c1 * (a.x - bb.y), c1 * (bb.x + a.y));
+      };
+      auto hi = [&](const double2& a, const double2& bb) {  // Zin_{M-j}
+        return make_double2(c1 * (a.x + bb.y), c1 * (a.y - bb.x));
+      };
+      if (!q0) {
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          // pair: slot (0, s) holds k0 = q + s NB, slot (1, 7-s) holds M - k0
+          const int j = s < 4 ? mirror::slot_k<M>(q, 0, s) : mirror::slot_k<M>(q, 1, 7 - s);
+          double2 a, bb;
+          rows(j, a, bb);
+          if (s < 4) {
+            v[s] = lo(a, bb);
+            v[8 + 7 - s] = hi(a, bb);
+          } else {
+            v[8 + 7 - s] = lo(a, bb);
+            v[s] = hi(a, bb);
+          }
+        }
+      } else {
+        // q == 0: butterflies 0 and NB/2 are self-mirrored
+        const double2 r0 = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 0, c);
+        const double2 r1 = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 1, c);
+        v[0] = make_double2(c0 * r0.x, c0 * r0.y);
+        v[4] = make_double2(c0 * r1.x, c0 * r1.y);
+#pragma unroll
+        for (int s = 1; s < 4; ++s) {
+          double2 a, bb;
+          rows(mirror::slot_k<M>(0, 0, s), a, bb);
+          v[s] = lo(a, bb);
+          v[8 - s] = hi(a, bb);
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          double2 a, bb;
+          rows(mirror::slot_k<M>(0, 1, s), a, bb);
+          v[8 + s] = lo(a, bb);
+          v[8 + 7 - s] = hi(a, bb);
+        }
+      }
+    }
+    refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
+    // mask bits of the 16 slots (x: bit 2i, y: bit 2i+1) packed into one
+    // register before the inverse FFT, so no mask word stays live across it
+    uint32_t mbits = 0;
+    if constexpr (KIND == K_GRAM || KIND == K_RESID) {
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int64_t t = mirror::slot_k<M>(q, i >> 3, i & 7);
+          const int64_t vx = Q.bx + t * Q.st;
+          mbits |= ((__ldg(A.bits + (vx >> 5)) >> (vx & 31)) & 1u) << (2 * i);
+          if (Q.by >= 0) {
+            const int64_t vy = Q.by + t * Q.st;
+            mbits |= ((__ldg(A.bits + (vy >> 5)) >> (vy & 31)) & 1u) << (2 * i + 1);
+          }
+        }
+      }
+    }
+    if (KIND == K_ANALYZE) {
+      mirror::fft<M>(v, fib, q, tw, -1);
+    } else {
+      mirror::fft<M>(v, fib, q, tw, +1);
+      if (KIND == K_SYNTH) {
+        if (valid) {
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              const int64_t t = mirror::slot_k<M>(q, b, s);
+              if (STRIDED) *reinterpret_cast<double2*>(A.out + Q.bx + t * Q.st) = v[8 * b + s];
+              else {
+                A.out[Q.bx + t] = v[8 * b + s].x;
+                if (Q.by >= 0) A.out[Q.by + t] = v[8 * b + s].y;
+              }
+            }
+        }
+      } else {
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            double2 z = v[8 * b + s];
+            if (valid) {
+              const int64_t t = mirror::slot_k<M>(q, b, s);
+              const int64_t vx = Q.bx + t * Q.st;
+              const bool mx = (mbits >> (2 * (8 * b + s))) & 1u;
+              if (KIND == K_RESID) z.x = mx ? 0.0 : A.bhat[vx] - z.x;
+              else if (mx) z.x = 0.0;
+              if (Q.by >= 0) {
+                const int64_t vy = Q.by + t * Q.st;
+                const bool my = (mbits >> (2 * (8 * b + s) + 1)) & 1u;
+                if (KIND == K_RESID) z.y = my ? 0.0 : A.bhat[vy] - z.y;
+                else if (my) z.y = 0.0;
+              } else {
+                z.y = 0.0;
+              }
+              if (KIND == K_GRAM) nrm += z.x * z.x + z.y * z.y;
+            }
+            v[8 * b + s] = z;
+          }
+        mirror::fft<M>(v, fib, q, tw, -1);
+      }
+    }
+    if (KIND != K_SYNTH && valid) {
+      // pack (Z_k, Z_{M-k}) straight from registers for the 8 slots with k < H
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const int j = mirror::slot_k<M>(q, b, s);
+          const double2 a = v[8 * b + s];
+          double xa, xb, ya, yb;
+          int64_t ia, ib;
+          if (b == 0 && s == 0 && q0) {
+            const double2 zh = v[4];  // Z_H of q = 0
+            xa = c0 * a.x; ya = c0 * a.y;
+            xb = c0 * zh.x; yb = c0 * zh.y;
+            ia = 0;
+            ib = Q.st;
+          } else {
+            // mirror partner of slot (b, s) (indices are constants after unrolling)
+            const double2 m = q0 ? v[8 * b + (b == 0 ? ((8 - s) & 7) : (7 - s))] : v[8 * (1 - b) + 7 - s];
+            xa = c1 * (a.x + m.x);
+            xb = c1 * (a.y - m.y);
+            ya = c1 * (a.y + m.y);
+            yb = c1 * (m.x - a.x);
+            ia = Q.st * (j + 1);
+            ib = Q.st * (j + H);
+          }
+          if (STRIDED && !EPI) {
+            *reinterpret_cast<double2*>(A.out + Q.bx + ia) = make_double2(xa, ya);
+            *reinterpret_cast<double2*>(A.out + Q.bx + ib) = make_double2(xb, yb);
+          } else if (STRIDED) {
+            kkt_store2(A, Q.bx + ia, xa, ya, acc);
+            kkt_store2(A, Q.bx + ib, xb, yb, acc);
+          } else {
+            put<STRIDED, EPI>(A, Q.bx + ia, xa, acc);
+            put<STRIDED, EPI>(A, Q.bx + ib, xb, acc);
+            if (Q.by >= 0) {
+              put<STRIDED, EPI>(A, Q.by + ia, ya, acc);
+              put<STRIDED, EPI>(A, Q.by + ib, yb, acc);
+            }
+          }
+        }
+    }
+  }
+  if (PIPE > 0) cp_wait<0>();
+  if (EPI && A.epi.partials) {
+    const double s = block_reduce(acc, SumOp(), red);
+    if (threadIdx.x == 0) A.epi.partials[blockIdx.x] = s;
+  }
+  if (KIND == K_GRAM && A.nrm_partials) {
+    const double s = block_reduce(nrm, SumOp(), red);
+    if (threadIdx.x == 0) A.nrm_partials[blockIdx.x] = s;
+  }
+}
+
+struct Entry {
+  KernelFn fn = nullptr;
+  int threads = 0, smem = 0, w = 0;
+};
+
+template <int M, bool S, int CFG>
+Entry make_cfg(int kind, bool epi) {
+  Entry e;
+  using G = Geom<M, CFG>;
+  switch (kind) {
+    case K_COPY: e.fn = fast_pass<M, S, K_COPY, false, CFG>; break;
+    case K_SYNTH: e.fn = fast_pass<M, S, K_SYNTH, false, CFG>; break;
+    case K_ANALYZE:
+      e.fn = epi ? fast_pass<M, S, K_ANALYZE, true, CFG> : fast_pass<M, S, K_ANALYZE, false, CFG>;
+      break;
+    case K_GRAM:
+      if constexpr (!S)
+        e.fn = epi ? fast_pass<M, false, K_GRAM, true, CFG> : fast_pass<M, false, K_GRAM, false, CFG>;
+      break;
+    default:
+      if constexpr (!S)
+        e.fn = epi ? fast_pass<M, false, K_RESID, true, CFG> : fast_pass<M, false, K_RESID, false, CFG>;
+      break;
+  }
+  e.threads = G::T;
+  e.smem = G::SMEM;
+  e.w = G::W;
+  return e;
+}
+
+// Default variant: plain strided passes on 512-thread CTAs without staging
+// (2 CTAs/SM at 64 registers); the fused gram pass and anything with an
+// epilogue on 256-thread CTAs with single-buffer cp.async staging (tools/
+// sweep_cfg.py on B200: 0.80 ms vs 0.92 double-buffered for the 512^3 gram pass).
+constexpr int kCfgLight = cfg_code(1, 0, 2);
+constexpr int kCfgHeavy = cfg_code(0, 1, 2);
+
+// Experiment hook (M = 512 only): FL_CFG_STRIDED / FL_CFG_CONTIG pick one of
+// the instantiated variants below for every plain-strided / other pass.
+template <bool S>
+Entry make512(int kind, bool epi, int cfg) {
+  switch (cfg) {
+    case cfg_code(1, 0, 2): return make_cfg<512, S, cfg_code(1, 0, 2)>(kind, epi);
+    case cfg_code(0, 1, 3): return make_cfg<512, S, cfg_code(0, 1, 3)>(kind, epi);
+    case cfg_code(0, 2, 2): return make_cfg<512, S, cfg_code(0, 2, 2)>(kind, epi);
+    case cfg_code(1, 1, 1): return make_cfg<512, S, cfg_code(1, 1, 1)>(kind, epi);
+    case cfg_code(1, 2, 1): return make_cfg<512, S, cfg_code(1, 2, 1)>(kind, epi);
+    case cfg_code(0, 0, 3): return make_cfg<512, S, cfg_code(0, 0, 3)>(kind, epi);
+    case cfg_code(0, 1, 2): return make_cfg<512, S, cfg_code(0, 1, 2)>(kind, epi);
+    case cfg_code(0, 0, 2, 1): return make_cfg<512, S, cfg_code(0, 0, 2, 1)>(kind, epi);
+    case cfg_code(0, 1, 2, 1): return make_cfg<512, S, cfg_code(0, 1, 2, 1)>(kind, epi);
+    case cfg_code(1, 0, 1, 1): return make_cfg<512, S, cfg_code(1, 0, 1, 1)>(kind, epi);
+    default: return Entry();
+  }
+}
+
+inline int env_cfg(const char* name) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : -1;
+}
+
+template <int M, bool S, int PIPE>
+Entry make_mirror(int kind, bool epi) {
+  Entry e;
+  using G = mirror::MGeom<M>;
+  switch (kind) {
+    case K_SYNTH: e.fn = mirror_pass<M, S, K_SYNTH, false, PIPE>; break;
+    case K_ANALYZE:
+      e.fn = epi ? mirror_pass<M, S, K_ANALYZE, true, PIPE> : mirror_pass<M, S, K_ANALYZE, false, PIPE>;
+      break;
+    case K_GRAM:
+      if constexpr (!S)
+        e.fn = epi ? mirror_pass<M, false, K_GRAM, true, PIPE> : mirror_pass<M, false, K_GRAM, false, PIPE>;
+      break;
+    case K_RESID:
+      if constexpr (!S)
+        e.fn = epi ? mirror_pass<M, false, K_RESID, true, PIPE> : mirror_pass<M, false, K_RESID, false, PIPE>;
+      break;
+    default: break;
+  }
+  e.threads = G::T;
+  e.smem = G::FIB_BYTES + PIPE * G::STAGE_BYTES;
+  e.w = G::W;
+  return e;
+}
+
+// FL_MIRROR: 0 off, 1 staging per kind (light passes direct, others single
+// cp.async buffer), 2 no staging, 3 single staging for every kind,
+// 4 (default) plain strided synthesis/analysis only, no staging -- the
+// measured best (tools/sweep_cfg.py); the fused gram pass keeps the E=8 engine.
+inline int mirror_mode() {
+  const char* v = std::getenv("FL_MIRROR");
+  return v ? std::atoi(v) : 4;
+}
+
+template <int M, bool S>
+Entry make(int kind, bool epi) {
+  const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE || kind == K_COPY);
+  if constexpr (M == 64 || M == 512 || M == 4096) {
+    int mm = kind == K_COPY ? 0 : mirror_mode();
+    if (mm == 4) mm = light ? 2 : 0;
+    if (mm > 0) {
+      const bool pipe = mm == 3 || (mm == 1 && !light);
+      Entry e = pipe ? make_mirror<M, S, 1>(kind, epi) : make_mirror<M, S, 0>(kind, epi);
+      if (e.fn) return e;
+    }
+  }
+  if constexpr (M == 512) {
+    const int over_s = env_cfg("FL_CFG_STRIDED"), over_c = env_cfg("FL_CFG_CONTIG");
+    const int over = light ? over_s : over_c;
+    if (over >= 0) {
+      Entry e = make512<S>(kind, epi, over);
+      if (e.fn) return e;
+    }
+  }
+  if constexpr (M <= 512) {
+    if (light) return make_cfg<M, S, kCfgLight>(kind, epi);
+  }
+  return make_cfg<M, S, kCfgHeavy>(kind, epi);
+}
+
+
+template <int M>
+Entry make_any(bool strided, int kind, bool epi) {
+  return strided ? make<M, true>(kind, epi) : make<M, false>(kind, epi);
+}
+
+}  // namespace fpk
+}  // namespace fl
