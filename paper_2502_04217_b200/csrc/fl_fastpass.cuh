@@ -371,8 +371,8 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
 // read the mirror partner from the thread's own registers, so a pass needs only
 // the NST-1 inter-stage shared-memory exchanges.
 // ---------------------------------------------------------------------------
-template <int M, bool STRIDED, int KIND, bool EPI, int PIPE>
-__global__ void __launch_bounds__(mirror::MGeom<M>::T, 2) mirror_pass(const PassArgs A) {
+template <int M, bool STRIDED, int KIND, bool EPI, int PIPE, int MB = 2>
+__global__ void __launch_bounds__(mirror::MGeom<M>::T, MB) mirror_pass(const PassArgs A) {
   using G = mirror::MGeom<M>;
   constexpr int CFG = cfg_code(0, PIPE, 2, 1);  // staging geometry shared with Geom<M, CFG>
   static_assert(Geom<M, CFG>::P == G::P && Geom<M, CFG>::W == G::W, "staging geometry mismatch");
@@ -637,22 +637,22 @@ inline int env_cfg(const char* name) {
   return v ? std::atoi(v) : -1;
 }
 
-template <int M, bool S, int PIPE>
+template <int M, bool S, int PIPE, int MB = 2>
 Entry make_mirror(int kind, bool epi) {
   Entry e;
   using G = mirror::MGeom<M>;
   switch (kind) {
-    case K_SYNTH: e.fn = mirror_pass<M, S, K_SYNTH, false, PIPE>; break;
+    case K_SYNTH: e.fn = mirror_pass<M, S, K_SYNTH, false, PIPE, MB>; break;
     case K_ANALYZE:
-      e.fn = epi ? mirror_pass<M, S, K_ANALYZE, true, PIPE> : mirror_pass<M, S, K_ANALYZE, false, PIPE>;
+      e.fn = epi ? mirror_pass<M, S, K_ANALYZE, true, PIPE, MB> : mirror_pass<M, S, K_ANALYZE, false, PIPE, MB>;
       break;
     case K_GRAM:
       if constexpr (!S)
-        e.fn = epi ? mirror_pass<M, false, K_GRAM, true, PIPE> : mirror_pass<M, false, K_GRAM, false, PIPE>;
+        e.fn = epi ? mirror_pass<M, false, K_GRAM, true, PIPE, MB> : mirror_pass<M, false, K_GRAM, false, PIPE, MB>;
       break;
     case K_RESID:
       if constexpr (!S)
-        e.fn = epi ? mirror_pass<M, false, K_RESID, true, PIPE> : mirror_pass<M, false, K_RESID, false, PIPE>;
+        e.fn = epi ? mirror_pass<M, false, K_RESID, true, PIPE, MB> : mirror_pass<M, false, K_RESID, false, PIPE, MB>;
       break;
     default: break;
   }
@@ -665,7 +665,10 @@ Entry make_mirror(int kind, bool epi) {
 // FL_MIRROR: 0 off, 1 staging per kind (light passes direct, others single
 // cp.async buffer), 2 no staging, 3 single staging for every kind,
 // 4 (default) plain strided synthesis/analysis only, no staging -- the
-// measured best (tools/sweep_cfg.py); the fused gram pass keeps the E=8 engine.
+// measured best (tools/sweep_cfg.py); the fused gram pass keeps the E=8 engine;
+// 5/6 as 4 plus the gram/residual pass on the mirrored engine with one
+// 256-thread CTA per SM (255 registers, no spills) and single (5) or no (6)
+// staging.
 inline int mirror_mode() {
   const char* v = std::getenv("FL_MIRROR");
   return v ? std::atoi(v) : 4;
@@ -676,7 +679,13 @@ Entry make(int kind, bool epi) {
   const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE || kind == K_COPY);
   if constexpr (M == 64 || M == 512 || M == 4096) {
     int mm = kind == K_COPY ? 0 : mirror_mode();
-    if (mm == 4) mm = light ? 2 : 0;
+    if ((mm == 5 || mm == 6) && !light && (kind == K_GRAM || kind == K_RESID)) {
+      if constexpr (M == 512) {
+        Entry e = mm == 5 ? make_mirror<M, S, 1, 1>(kind, epi) : make_mirror<M, S, 0, 1>(kind, epi);
+        if (e.fn) return e;
+      }
+    }
+    if (mm >= 4) mm = light ? 2 : 0;
     if (mm > 0) {
       const bool pipe = mm == 3 || (mm == 1 && !light);
       Entry e = pipe ? make_mirror<M, S, 1>(kind, epi) : make_mirror<M, S, 0>(kind, epi);

@@ -40,7 +40,7 @@ def test_variant_matches_oracle(var, which, monkeypatch):
     _check_all_dims(var)
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "2", "3", "4"])
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3", "4", "5", "6"])
 def test_mirror_engine_matches_oracle(mode, monkeypatch):
     """The mirrored-butterfly engine (FL_MIRROR, m = 64 / 512 / 4096)."""
     monkeypatch.setenv("FL_MIRROR", mode)

@@ -69,7 +69,7 @@ def main():
             print(f"{which}={cfg:2d} {name:18s} passes_ms={np.round(ms, 4).tolist()} total={ms.sum():.4f} "
                   f"maxdiff={err:.1e}", flush=True)
         del os.environ[which]
-    for mm in ("0", "1", "2", "3", "4"):
+    for mm in ("0", "1", "2", "3", "4", "5", "6"):
         os.environ["FL_MIRROR"] = mm
         ms = run()
         err = float((top - ref).abs().max())
