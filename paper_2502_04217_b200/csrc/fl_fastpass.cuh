@@ -43,6 +43,27 @@ __device__ __forceinline__ void lane_map(int tid, int W, int P, int& c, int& q) 
   else { q = tid % P; c = tid / P; }          // position-fast: contiguous rows
 }
 
+// Contiguous layout with P = 64 threads per fibre (m = 512, E = 8): place q and
+// its pack partner 64 - q in the SAME warp so Z_{m-k} arrives by shuffle.
+//   warp A: lanes 0..15 -> q 0..15, lane 16 -> q 32, lanes 17..31 -> q 49..63
+//   warp B: lanes 0..15 -> q 16..31, lanes 16..31 -> q 33..48
+// partner lane: warp A (lane == 0 || lane == 16) ? lane : 32 - lane; warp B 31 - lane.
+__device__ __forceinline__ void lane_map_pair64(int tid, int& c, int& q, int& partner) {
+  c = tid >> 6;
+  const int l = tid & 63, w = l >> 5, lane = l & 31;
+  if (w == 0) {
+    q = lane < 16 ? lane : (lane == 16 ? 32 : 32 + lane);
+    partner = (lane == 0 || lane == 16) ? lane : 32 - lane;
+  } else {
+    q = lane < 16 ? 16 + lane : 17 + lane;
+    partner = 31 - lane;
+  }
+}
+
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
 // 16-byte KKT epilogue for a strided-axis pair (x at v, y at v + 1).
 __device__ __forceinline__ void kkt_store2(const PassArgs& A, int64_t v, double gx, double gy,
                                            double& acc) {
@@ -130,8 +151,11 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
   constexpr int PIPE = G::PIPE;  // 0 none, 1 single, 2 double buffered staging
   extern __shared__ double2 smem[];
   __shared__ double red[32];
-  int c, q;
-  lane_map<STRIDED>(threadIdx.x, W, P, c, q);
+  // pack partner by warp shuffle (contiguous layout, 64 threads per fibre)
+  constexpr bool SHFL_PACK = !STRIDED && P == 64 && E == 8;
+  int c, q, partner = 0;
+  if constexpr (SHFL_PACK) lane_map_pair64(threadIdx.x, c, q, partner);
+  else lane_map<STRIDED>(threadIdx.x, W, P, c, q);
   double2* fib = smem + c * G::FS;
   double2* stage0 = smem + G::FIB_BYTES / 16;
   double2* stage1 = stage0 + W * M;
@@ -314,7 +338,42 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
         fast::fft<M, CFG>(v, fib, q, tw, -1);
       }
     }
-    if (KIND != K_SYNTH) {
+    if (KIND != K_SYNTH && SHFL_PACK) {
+      // thread q holds Z_{q + 64 r}; its mirror Z_{512 - q - 64 r} is slot 7 - r of
+      // lane `partner` (q = 32: itself, slot 7 - r; q = 0: itself, slot (8 - r) & 7)
+      double2 mir[E / 2];
+#pragma unroll
+      for (int r = 0; r < E / 2; ++r) {
+        const double2 sh = shfl2(v[E - 1 - r], partner);
+        mir[r] = q == 0 ? v[(E - r) & (E - 1)] : sh;
+      }
+      if (valid) {
+#pragma unroll
+        for (int r = 0; r < E / 2; ++r) {
+          const int j = q + r * P;
+          const bool j0 = r == 0 && q == 0;
+          const double2 a = v[r], b = mir[r];
+          double xa, xb, ya, yb;
+          if (j0) {
+            const double2 zh = v[E / 2];
+            xa = c0 * a.x; ya = c0 * a.y;
+            xb = c0 * zh.x; yb = c0 * zh.y;
+          } else {
+            xa = c1 * (a.x + b.x);
+            xb = c1 * (a.y - b.y);
+            ya = c1 * (a.y + b.y);
+            yb = c1 * (b.x - a.x);
+          }
+          const int64_t ia = j0 ? 0 : j + 1, ib = j0 ? 1 : j + H;
+          put<STRIDED, EPI>(A, Q.bx + ia, xa, acc);
+          put<STRIDED, EPI>(A, Q.bx + ib, xb, acc);
+          if (Q.by >= 0) {
+            put<STRIDED, EPI>(A, Q.by + ia, ya, acc);
+            put<STRIDED, EPI>(A, Q.by + ib, yb, acc);
+          }
+        }
+      }
+    } else if (KIND != K_SYNTH) {
       fast::store_natural<M, CFG>(v, fib, q);
       __syncthreads();
       if (valid) {
