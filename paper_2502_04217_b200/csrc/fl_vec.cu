@@ -523,6 +523,23 @@ __global__ void k_pcg2_init(int64_t n, const double* __restrict__ g1, const doub
 
 // x += alpha p; r -= alpha K p with K p formed in registers from g = G p_beta
 // exactly as apply_kkt (newton_system.py:150-151); z = P^{-1} r; rho partials.
+// 16-byte accesses: each thread handles voxels (2i, 2i+1) of both blocks.
+struct KUpd {
+  __device__ __forceinline__ static void one(double a1, double a2, double alpha, double g, double pt,
+                                             double pb, double& xt, double& xb, double& rt, double& rb,
+                                             double& rho) {
+    const double l1 = add(a1, a2), l2 = sub(a1, a2);
+    const double kt = add(add(g, mul(l1, pt)), mul(l2, pb));
+    const double kb = add(mul(l2, pt), mul(l1, pb));
+    xt = add(xt, mul(alpha, pt));
+    xb = add(xb, mul(alpha, pb));
+    rt = sub(rt, mul(alpha, kt));
+    rb = sub(rb, mul(alpha, kb));
+    const Pinv P(a1, a2);
+    rho += mul(rt, P.top(rt, rb)) + mul(rb, P.bot(rt, rb));
+  }
+};
+
 __global__ void k_pcg2_update(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
                               const double* __restrict__ rho_p, const double* __restrict__ curv_g,
                               const double* __restrict__ curv_d, double* __restrict__ x,
@@ -531,20 +548,25 @@ __global__ void k_pcg2_update(int64_t n, const double* __restrict__ g1, const do
   __shared__ double red[32];
   const double alpha = dvd(*rho_p, add(*curv_g, *curv_d));
   double rho = 0.0;
-  GRID_LOOP(i, n) {
-    const double pt = p[i], pb = p[n + i];
-    const double a1 = g1[i], a2 = g2[i];
-    const double l1 = add(a1, a2), l2 = sub(a1, a2);
-    const double kt = add(add(gp[i], mul(l1, pt)), mul(l2, pb));
-    const double kb = add(mul(l2, pt), mul(l1, pb));
-    x[i] = add(x[i], mul(alpha, pt));
-    x[n + i] = add(x[n + i], mul(alpha, pb));
-    const double rt = sub(r[i], mul(alpha, kt));
-    const double rb = sub(r[n + i], mul(alpha, kb));
-    r[i] = rt;
-    r[n + i] = rb;
-    const Pinv P(a1, a2);
-    rho += mul(rt, P.top(rt, rb)) + mul(rb, P.bot(rt, rb));
+  const int64_t n2 = n >> 1;
+  const double2* G1 = reinterpret_cast<const double2*>(g1);
+  const double2* G2 = reinterpret_cast<const double2*>(g2);
+  const double2* PT = reinterpret_cast<const double2*>(p);
+  const double2* PB = reinterpret_cast<const double2*>(p + n);
+  const double2* GP = reinterpret_cast<const double2*>(gp);
+  double2* XT = reinterpret_cast<double2*>(x);
+  double2* XB = reinterpret_cast<double2*>(x + n);
+  double2* RT = reinterpret_cast<double2*>(r);
+  double2* RB = reinterpret_cast<double2*>(r + n);
+  GRID_LOOP(i, n2) {
+    const double2 a1 = G1[i], a2 = G2[i], pt = PT[i], pb = PB[i], g = GP[i];
+    double2 xt = XT[i], xb = XB[i], rt = RT[i], rb = RB[i];
+    KUpd::one(a1.x, a2.x, alpha, g.x, pt.x, pb.x, xt.x, xb.x, rt.x, rb.x, rho);
+    KUpd::one(a1.y, a2.y, alpha, g.y, pt.y, pb.y, xt.y, xb.y, rt.y, rb.y, rho);
+    XT[i] = xt;
+    XB[i] = xb;
+    RT[i] = rt;
+    RB[i] = rb;
   }
   emit(rho, SumOp(), red, partials, 0);
 }
@@ -554,14 +576,30 @@ __global__ void k_pcg2_pupdate(int64_t n, const double* __restrict__ g1, const d
                                double* __restrict__ partials) {
   __shared__ double red[32];
   double dq = 0.0;
-  GRID_LOOP(i, n) {
-    const double rt = r[i], rb = r[n + i];
-    const Pinv P(g1[i], g2[i]);
-    const double pt = add(P.top(rt, rb), mul(beta, p[i]));
-    const double pb = add(P.bot(rt, rb), mul(beta, p[n + i]));
-    p[i] = pt;
-    p[n + i] = pb;
-    dq += diag_quad(P.l1, P.l2, pt, pb);
+  const int64_t n2 = n >> 1;
+  const double2* G1 = reinterpret_cast<const double2*>(g1);
+  const double2* G2 = reinterpret_cast<const double2*>(g2);
+  const double2* RT = reinterpret_cast<const double2*>(r);
+  const double2* RB = reinterpret_cast<const double2*>(r + n);
+  double2* PT = reinterpret_cast<double2*>(p);
+  double2* PB = reinterpret_cast<double2*>(p + n);
+  GRID_LOOP(i, n2) {
+    const double2 a1 = G1[i], a2 = G2[i], rt = RT[i], rb = RB[i];
+    double2 pt = PT[i], pb = PB[i];
+    {
+      const Pinv P(a1.x, a2.x);
+      pt.x = add(P.top(rt.x, rb.x), mul(beta, pt.x));
+      pb.x = add(P.bot(rt.x, rb.x), mul(beta, pb.x));
+      dq += diag_quad(P.l1, P.l2, pt.x, pb.x);
+    }
+    {
+      const Pinv P(a1.y, a2.y);
+      pt.y = add(P.top(rt.y, rb.y), mul(beta, pt.y));
+      pb.y = add(P.bot(rt.y, rb.y), mul(beta, pb.y));
+      dq += diag_quad(P.l1, P.l2, pt.y, pb.y);
+    }
+    PT[i] = pt;
+    PB[i] = pb;
   }
   emit(dq, SumOp(), red, partials, 0);
 }
@@ -661,6 +699,7 @@ int pcg2_init(int64_t n, const double* sig1, const double* sig2, const double* r
 int pcg2_update(int64_t n, const double* sig1, const double* sig2, const double* rho, const double* curv_g,
                 const double* curv_d, double* x, double* r, const double* p, const double* gp,
                 double* partials, int* nblocks, cudaStream_t s) {
+  if (n % 2) return fail(FL_E_SHAPE, "PCG update needs an even length (16-byte accesses)");
   const int grid = grid_for(n, T);
   k_pcg2_update<<<grid, T, 0, s>>>(n, sig1, sig2, rho, curv_g, curv_d, x, r, p, gp, partials);
   FL_LAUNCH_CHECK();
@@ -670,6 +709,7 @@ int pcg2_update(int64_t n, const double* sig1, const double* sig2, const double*
 
 int pcg2_pupdate(int64_t n, const double* sig1, const double* sig2, const double* r, double beta, double* p,
                  double* partials, int* nblocks, cudaStream_t s) {
+  if (n % 2) return fail(FL_E_SHAPE, "PCG p-update needs an even length (16-byte accesses)");
   const int grid = grid_for(n, T);
   k_pcg2_pupdate<<<grid, T, 0, s>>>(n, sig1, sig2, r, beta, p, partials);
   FL_LAUNCH_CHECK();
