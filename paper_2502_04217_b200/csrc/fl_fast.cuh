@@ -16,12 +16,23 @@
 // stride-R write of the first stage.  Both layouts are conflict-free.
 #pragma once
 
+#include <type_traits>
+
 #include "fl_fft.cuh"
 
 namespace fl {
 namespace fast {
 
 __device__ __forceinline__ int si(int k) { return k + (k >> 3); }
+
+// Compile-time loop: f(std::integral_constant<int, I>{}) for I in [B, E).
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
 
 constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 constexpr int nfull(int m, int e) { return (m % e == 0 && m > 1) ? 1 + nfull(m / e, e) : 0; }
