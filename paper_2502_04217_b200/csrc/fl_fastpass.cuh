@@ -481,48 +481,42 @@ __global__ void __launch_bounds__(mirror::MGeom<M>::T, MB) mirror_pass(const Pas
       auto hi = [&](const double2& a, const double2& bb) {  // Zin_{M-j}
         return make_double2(c1 * (a.x + bb.y), c1 * (a.y - bb.x));
       };
-      // Branch-free over q: iteration s handles one mirror pair for every lane.
-      //   q != 0: slots (0, s) <-> (1, 7 - s)
-      //   q == 0: s = 0 DC/Nyquist (rows 0 and 1 -> slots (0,0), (0,4)),
-      //           s = 1..3 (0, s) <-> (0, 8 - s), s = 4..7 (1, s-4) <-> (1, 11 - s)
-      // Destinations differ per lane type; they are selected on compile-time
-      // register indices, so warp 0 no longer diverges (and stalls its CTA).
-      constexpr int NB = G::NB;
+      if (!q0) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = make_double2(0.0, 0.0);
-      auto pair_s = [&](auto sc) {
-        constexpr int s = decltype(sc)::value;
-        const int jg = s < 4 ? mirror::slot_k<M>(q, 0, s) : mirror::slot_k<M>(q, 1, 7 - s);
-        const int j0 = s < 4 ? s * NB : NB / 2 + (s - 4) * NB;
-        const bool dc = q0 && s == 0;
-        const int j = q0 ? j0 : jg;
-        double2 a, bb;
-        if (dc) {
-          a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 0, c);
-          bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 1, c);
-        } else {
+        for (int s = 0; s < 8; ++s) {
+          // pair: slot (0, s) holds k0 = q + s NB, slot (1, 7-s) holds M - k0
+          const int j = s < 4 ? mirror::slot_k<M>(q, 0, s) : mirror::slot_k<M>(q, 1, 7 - s);
+          double2 a, bb;
           rows(j, a, bb);
+          if (s < 4) {
+            v[s] = lo(a, bb);
+            v[8 + 7 - s] = hi(a, bb);
+          } else {
+            v[8 + 7 - s] = lo(a, bb);
+            v[s] = hi(a, bb);
+          }
         }
-        const double2 zlo = dc ? make_double2(c0 * a.x, c0 * a.y) : lo(a, bb);
-        const double2 zhi = dc ? make_double2(c0 * bb.x, c0 * bb.y) : hi(a, bb);
-        constexpr int gl = s < 4 ? s : 8 + 7 - s;  // generic slot of Zin_j
-        constexpr int gh = s < 4 ? 8 + 7 - s : s;  // generic slot of Zin_{M-j}
-        constexpr int zl = s == 0 ? 0 : (s < 4 ? s : 8 + (s - 4));       // q == 0 slots
-        constexpr int zh = s == 0 ? 4 : (s < 4 ? 8 - s : 8 + 11 - s);
-        if constexpr (gl == zl) {
-          v[gl] = zlo;
-        } else {
-          v[gl] = q0 ? v[gl] : zlo;
-          v[zl] = q0 ? zlo : v[zl];
+      } else {
+        // q == 0: butterflies 0 and NB/2 are self-mirrored
+        const double2 r0 = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 0, c);
+        const double2 r1 = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 1, c);
+        v[0] = make_double2(c0 * r0.x, c0 * r0.y);
+        v[4] = make_double2(c0 * r1.x, c0 * r1.y);
+#pragma unroll
+        for (int s = 1; s < 4; ++s) {
+          double2 a, bb;
+          rows(mirror::slot_k<M>(0, 0, s), a, bb);
+          v[s] = lo(a, bb);
+          v[8 - s] = hi(a, bb);
         }
-        if constexpr (gh == zh) {
-          v[gh] = zhi;
-        } else {
-          v[gh] = q0 ? v[gh] : zhi;
-          v[zh] = q0 ? zhi : v[zh];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          double2 a, bb;
+          rows(mirror::slot_k<M>(0, 1, s), a, bb);
+          v[8 + s] = lo(a, bb);
+          v[8 + 7 - s] = hi(a, bb);
         }
-      };
-      fast::static_for<0, 8>(pair_s);
+      }
     }
     refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
     // mask bits of the 16 slots (x: bit 2i, y: bit 2i+1) packed into one
