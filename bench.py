@@ -496,6 +496,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=150.0)
     ap.add_argument("--emulate", type=int, default=0,
                     help="run the sharded (N>1) code path with P emulated ranks on one GPU")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded path (torch.distributed + NCCL) even at one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 
@@ -511,10 +513,10 @@ def main():
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1 or args.emulate > 1:
+    if world > 1 or args.emulate > 1 or args.sharded:
         from paper_2502_04217_b200 import sharded as sh
 
-        if world > 1:
+        if world > 1 or args.sharded:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             comm = sh.DistComm(device=torch.device("cuda", local))
 
