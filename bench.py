@@ -550,7 +550,7 @@ def main():
                 "config": {"workload": f"slab-sharded KKT matvec, global grid {res['dims']} "
                                        f"({args.size}^3 voxels per GPU; P={P}: 5 HBM passes + 2 all-to-all "
                                        "transposes + epilogue per matvec)",
-                           "n": n_all, "parallelism": f"slab x{P}" + (" (emulated on 1 GPU)" if world == 1 else ""),
+                           "n": n_all, "parallelism": f"slab x{P}" + (" (emulated on 1 GPU)" if isinstance(comm, sh.LocalComm) else ""),
                            "l2": "inputs >> 126 MB L2"},
                 "roofline": {"bound": "hbm", "achieved": round(120.125 * n_all / P / (res["ms"] / args.steps * 1e6), 1),
                              "peak": peak, "unit": "GB/s",

@@ -522,7 +522,22 @@ __global__ void __launch_bounds__(mirror::MGeom<M>::T, MB) mirror_pass(const Pas
     // mask bits of the 16 slots (x: bit 2i, y: bit 2i+1) packed into one
     // register before the inverse FFT, so no mask word stays live across it
     uint32_t mbits = 0;
-    if constexpr (KIND == K_GRAM || KIND == K_RESID) {
+    if constexpr ((KIND == K_GRAM || KIND == K_RESID) && !STRIDED && P == 32) {
+      // one warp = one row pair of 512 samples = 2 x 16 mask words: lane l
+      // loads word l & 15 of row x (l < 16) or row y, slots fetch theirs by
+      // shuffle (one live register instead of 32 in-flight word loads)
+      const int l = threadIdx.x & 31;
+      uint32_t word = 0;
+      if (valid && (l < 16 || Q.by >= 0)) word = __ldg(A.bits + (((l < 16) ? Q.bx : Q.by) >> 5) + (l & 15));
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int t = mirror::slot_k<M>(q, i >> 3, i & 7);
+        const uint32_t wx = __shfl_sync(0xffffffffu, word, t >> 5);
+        const uint32_t wy = __shfl_sync(0xffffffffu, word, 16 + (t >> 5));
+        mbits |= ((wx >> (t & 31)) & 1u) << (2 * i);
+        mbits |= ((wy >> (t & 31)) & 1u) << (2 * i + 1);
+      }
+    } else if constexpr (KIND == K_GRAM || KIND == K_RESID) {
       if (valid) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -536,10 +551,14 @@ __global__ void __launch_bounds__(mirror::MGeom<M>::T, MB) mirror_pass(const Pas
         }
       }
     }
+    // twiddle loads are loop invariant; laundering the table pointer per FFT
+    // keeps the compiler from hoisting/CSE-ing them into ~100 live registers
+    const double2* tw1 = tw;
+    asm volatile("" : "+l"(tw1));
     if (KIND == K_ANALYZE) {
-      mirror::fft<M>(v, fib, q, tw, -1);
+      mirror::fft<M>(v, fib, q, tw1, -1);
     } else {
-      mirror::fft<M>(v, fib, q, tw, +1);
+      mirror::fft<M>(v, fib, q, tw1, +1);
       if (KIND == K_SYNTH) {
         if (valid) {
 #pragma unroll
@@ -578,7 +597,9 @@ __global__ void __launch_bounds__(mirror::MGeom<M>::T, MB) mirror_pass(const Pas
             }
             v[8 * b + s] = z;
           }
-        mirror::fft<M>(v, fib, q, tw, -1);
+        const double2* tw2 = tw;
+        asm volatile("" : "+l"(tw2));
+        mirror::fft<M>(v, fib, q, tw2, -1);
       }
     }
     if (KIND != K_SYNTH && valid) {
