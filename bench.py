@@ -360,7 +360,7 @@ def make_kkt_inputs_n(n: int, seed: int = 0):
     return sig1, sig2, torch.randn(2 * n, dtype=torch.float64, device="cuda", generator=gen)
 
 
-def _solve_instance(inst, barrier, reps_warm=1):
+def _solve_instance(inst, barrier, reps_warm=1, ista=False):
     """Cold + warm device solves and one NumPy-in/NumPy-out solve of a recipe instance."""
     import torch
 
@@ -384,6 +384,24 @@ def _solve_instance(inst, barrier, reps_warm=1):
         beta, rep = fl.solve(b, mask, cfg)
         barrier()
         warm.append(time.perf_counter() - t0)
+    cross = None
+    if ista:
+        # independent first-order oracle at full size: the
+        # unguarded GPU ISTA must reach the IPM objective within 1e-6
+        from paper_2502_04217_b200 import diagnostics as dg
+
+        t0 = time.perf_counter()
+        try:
+            ref, iters = dg.ista_solve(b, mask, rep.lam, tol=1e-10, max_iters=3000, max_n=None)
+            o_ipm = fl.lasso_objective(beta, b, mask, rep.lam)
+            o_ista = fl.lasso_objective(ref, b, mask, rep.lam)
+            same = bool(np.array_equal(dg.classify_support(beta).active, dg.classify_support(ref).active))
+            cross = {"ista_iterations": iters, "ista_s": round(time.perf_counter() - t0, 3),
+                     "ipm_objective": o_ipm, "ista_objective": o_ista,
+                     "rel_diff": abs(o_ipm - o_ista) / abs(o_ista), "same_support": same}
+            del ref
+        except Exception as exc:  # report, never hide
+            cross = {"error": repr(exc)[:300]}
     b_host = b.cpu().numpy()
     del b, bt, beta
     torch.cuda.empty_cache()
@@ -397,14 +415,15 @@ def _solve_instance(inst, barrier, reps_warm=1):
             "krylov": rep.krylov_counts, "total_krylov": rep.total_krylov,
             "device_s_cold": round(cold, 4), "device_s": round(min(warm), 4), "e2e_s": round(e2e_s, 4),
             "final_objective": rep.final_objective,
-            "support_exact": bool(np.array_equal(found, true_support)), "n_support": int(found.size)}
+            "support_exact": bool(np.array_equal(found, true_support)), "n_support": int(found.size),
+            **({"ista_crosscheck": cross} if ista else {})}
 
 
 def run_solve(side: int, barrier):
     """Full IPM solve of the C4 recipe (lambda 0.5) at side^3."""
     from paper_2502_04217_b200 import workloads
 
-    out = _solve_instance(workloads.c4_const(side), barrier)
+    out = _solve_instance(workloads.c4_const(side), barrier, ista=True)
     out["config"] = f"C4 recipe {side}^3, lambda=0.5, tol=1e-8"
     return out
 

@@ -290,6 +290,16 @@ FL_API int fl_axpy(int64_t n, double alpha, const double* x, double* y, fl_strea
 /* y = x + beta * y    (NumPy ``p = z + beta * p``) */
 FL_API int fl_xpby(int64_t n, const double* x, double beta, double* y, fl_stream_t stream);
 
+/* ---- diagnostics (diagnostics.py) -------------------------------------- */
+/* out = sign(x) * max(|x| - t, 0) elementwise, NumPy conventions
+ * (soft_threshold, diagnostics.py:325-328); in place allowed. */
+FL_API int fl_soft_threshold(int64_t n, const double* x, double t, double* out, fl_stream_t stream);
+/* One ISTA iteration after the gram (ista_solve, diagnostics.py:352-357):
+ * next = soft(beta - (gram_beta - xi), lam); *step = max|next - beta| (host
+ * scalar, synchronises). */
+FL_API int fl_ista_step(int64_t n, const double* beta, const double* gram_beta, const double* xi,
+                        double lam, double* next, double* step, fl_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

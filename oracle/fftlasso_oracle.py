@@ -523,3 +523,40 @@ def solve(b, mask: OMask, cfg: OConfig = OConfig(), observer=None):
                   final_kkt=conv["max_residual"] if status == "converged" else best_kkt,
                   final_mu=st.mu, wall_time=time.perf_counter() - t0)
     return beta, rep
+
+
+# ---------------------------------------------------------------------------
+# diagnostics.py: soft threshold, support classification, ISTA cross-check
+# ---------------------------------------------------------------------------
+
+def soft_threshold(x, t: float) -> np.ndarray:
+    """diagnostics.py:325-328: sign(x) * max(|x| - t, 0)."""
+    x = np.asarray(x, dtype=np.float64)
+    return np.sign(x) * np.maximum(np.abs(x) - t, 0.0)
+
+
+def support(beta, threshold=None):
+    """diagnostics.py:129-142 -> (positive, negative, zero, threshold)."""
+    beta = np.asarray(beta, dtype=np.float64).reshape(-1)
+    if threshold is None:
+        threshold = 1e-6 * (float(np.max(np.abs(beta))) if beta.size else 0.0)
+    return (np.flatnonzero(beta > threshold), np.flatnonzero(beta < -threshold),
+            np.flatnonzero(np.abs(beta) <= threshold), float(threshold))
+
+
+def ista(b, mask: OMask, lam: float, tol: float = 1e-10, max_iters: int = 10**6):
+    """diagnostics.py:331-360 without the n <= 4096 guard -> (beta, iterations).
+
+    Unit-step proximal gradient: grad = G beta - xi, beta+ = soft(beta - grad,
+    lam), stop when max|beta+ - beta| <= tol; raises RuntimeError at the cap
+    (the reference raises IterationLimitError, a RuntimeError).
+    """
+    xi = observe_adjoint(np.asarray(b, dtype=np.float64).reshape(-1), mask)
+    beta = np.zeros(mask.n)
+    for k in range(1, max_iters + 1):
+        nxt = soft_threshold(beta - (gram(beta, mask) - xi), lam)
+        step = float(np.max(np.abs(nxt - beta))) if beta.size else 0.0
+        beta = nxt
+        if step <= tol:
+            return beta, k
+    raise RuntimeError(f"ISTA did not reach tol={tol:.1e} within {max_iters} iterations")

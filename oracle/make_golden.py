@@ -241,12 +241,113 @@ def solves():
     _record_solve("maxit_64", (64,), flags, b, 0.4, max_iters=3)
 
 
+def _sparse_1d(rng, n, n_missing, n_active, amplitude=(1.0, 2.0), noise=0.02):
+    """Masked sparse 1D instance (the reference tests' conftest recipe)."""
+    g = ref.GridShape((n,))
+    mask = ref.Mask(np.sort(rng.choice(n, size=n_missing, replace=False)), g)
+    beta = np.zeros(n)
+    idx = rng.choice(n, size=n_active, replace=False)
+    lo, hi = amplitude
+    beta[idx] = (lo + (hi - lo) * rng.random(n_active)) * np.sign(rng.standard_normal(n_active))
+    return ref.observe(beta, mask) + noise * rng.standard_normal(mask.n_observed), mask
+
+
+def ista():
+    """Reference diagnostics: soft_threshold and the ISTA oracle (diagnostics.py:325-360)."""
+    from fftlasso import diagnostics as ref_diag
+
+    x = np.concatenate([[0.0, -0.0, 0.3, -0.3, 0.30000000000000004, 1e300, -1e-300, np.inf, -np.inf],
+                        np.random.default_rng(11).standard_normal(64)])
+    arrays = dict(soft_x=x, soft_t=np.array(0.3), soft_out=ref_diag.soft_threshold(x, 0.3))
+    cases = []
+    rng = np.random.default_rng(3000)
+    b, mask = _sparse_1d(rng, 64, 10, 3, amplitude=(1.0, 2.5), noise=0.05)
+    cases.append(("c64", b, mask, 0.3))
+    rng = np.random.default_rng(3001)
+    b, mask = _sparse_1d(rng, 128, 19, 5, amplitude=(1.0, 2.5), noise=0.05)
+    cases.append(("c128", b, mask, 0.3))
+    rng = np.random.default_rng(3002)
+    g = ref.GridShape((16, 16))
+    flags = rng.random(256) < 0.12
+    m2 = ref.Mask.from_bool(flags, g)
+    bt = np.zeros(256)
+    bt[rng.choice(256, 6, replace=False)] = rng.uniform(1.0, 2.0, 6)
+    cases.append(("c16x16", ref.observe(bt, m2) + 0.03 * rng.standard_normal(m2.n_observed), m2, 0.25))
+    noisy, flags, _ = workloads.harmonics((8, 8, 8), noise_seed=42, missing_seed=43)
+    m3 = ref.Mask.from_bool(flags, ref.GridShape((8, 8, 8)))
+    b3 = noisy[~flags]
+    cases.append(("harm8", b3, m3, ref_ipm.default_penalty(b3, m3)))
+    names = []
+    for name, b, mask, lam in cases:
+        beta, iters = ref_diag.ista_solve(b, mask, lam, tol=1e-10)
+        om = orc.make_mask(mask.shape.dims, missing=mask.missing)
+        obeta, oiters = orc.ista(b, om, lam, tol=1e-10)
+        note("ista beta", beta, obeta)
+        assert oiters == iters, (name, oiters, iters)
+        arrays.update({f"{name}_dims": np.array(mask.shape.dims), f"{name}_missing": mask.missing,
+                       f"{name}_b": b, f"{name}_lam": np.array(lam), f"{name}_beta": beta,
+                       f"{name}_iters": np.array(iters),
+                       f"{name}_objective": np.array(ref_ipm.lasso_objective(beta, b, mask, lam))})
+        names.append(name)
+        print(f"    {name}: {iters} ISTA iterations, lam {lam:.4g}")
+    arrays["cases_json"] = np.array(json.dumps(names))
+    save("ista", **arrays)
+
+
+def _strip_wall(rows):
+    return [{k: v for k, v in r.items() if k != "wall_time"} for r in rows]
+
+
+def cli():
+    """The reference CLI end to end (cli.py:37-144): files, reports, exit codes."""
+    import tempfile
+
+    from fftlasso import cli as ref_cli
+
+    with tempfile.TemporaryDirectory() as tmp:
+        sig, msk, byt = (os.path.join(tmp, f) for f in ("signal.f64", "mask.idx", "mask.byte"))
+        beta, imp, rep = (os.path.join(tmp, f) for f in ("beta.f64", "imputed.f64", "report.jsonl"))
+        assert ref_cli.main(["generate", "--dims", "8,8,8", "--noise-seed", "3", "--missing-seed", "4",
+                             "--signal", sig, "--mask", msk]) == 0
+        assert ref_cli.main(["generate", "--dims", "8,8,8", "--noise-seed", "3", "--missing-seed", "4",
+                             "--signal", sig, "--mask", byt, "--mask-format", "bytemask"]) == 0
+        code = ref_cli.main(["solve", "--input", sig, "--mask", msk, "--output", beta,
+                             "--report", rep, "--impute", imp])
+        with open(rep) as fh:
+            records = [json.loads(line) for line in fh if line.strip()]
+        code_max = ref_cli.main(["solve", "--input", sig, "--mask", msk, "--max-iters", "2",
+                                 "--output", beta + ".2", "--report", rep + ".2"])
+        with open(rep + ".2") as fh:
+            records_max = [json.loads(line) for line in fh if line.strip()]
+        bench = os.path.join(tmp, "bench.jsonl")
+        code_bench = ref_cli.main(["bench", "--sizes", "4,8", "--seed", "7", "--report", bench])
+        with open(bench) as fh:
+            bench_rows = [json.loads(line) for line in fh if line.strip()]
+
+        def raw(path):
+            return np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+
+        def side(path):
+            return np.array(open(path + ".json").read())
+
+        save("cli_8", signal=raw(sig), signal_json=side(sig), mask_idx=raw(msk), mask_idx_json=side(msk),
+             mask_byte=raw(byt), mask_byte_json=side(byt), beta=raw(beta), imputed=raw(imp),
+             code=np.array(code), code_max=np.array(code_max), code_bench=np.array(code_bench),
+             records_json=np.array(json.dumps(_strip_wall(records))),
+             records_max_json=np.array(json.dumps(_strip_wall(records_max))),
+             bench_json=np.array(json.dumps(_strip_wall(bench_rows))))
+        print(f"    cli: solve exit {code}, {records[-1]['status']} in {records[-1]['iterations']}; "
+              f"max-iters exit {code_max}; bench exit {code_bench}")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    print("transforms");  transforms()
-    print("masking");     masking()
-    print("newton");      newton()
-    print("solves");      solves()
+    only = set(sys.argv[1:])
+    for name, fn in (("transforms", transforms), ("masking", masking), ("newton", newton),
+                     ("solves", solves), ("cli", cli), ("ista", ista)):
+        if not only or name in only:
+            print(name)
+            fn()
     print("oracle vs reference worst relative deviation:")
     for k, v in WORST.items():
         print(f"  {k:16s} {v:.3e}")

@@ -95,6 +95,8 @@ SIGNATURES = {
     "fl_ftb_ratio": (_I, [_I64, _P, _P, ctypes.POINTER(_D), _P]),
     "fl_axpy": (_I, [_I64, _D, _P, _P, _P]),
     "fl_xpby": (_I, [_I64, _P, _D, _P, _P]),
+    "fl_soft_threshold": (_I, [_I64, _P, _D, _P, _P]),
+    "fl_ista_step": (_I, [_I64, _P, _P, _P, _D, _P, ctypes.POINTER(_D), _P]),
 }
 
 _lock = threading.Lock()

@@ -57,6 +57,15 @@ struct MinOp {
   static constexpr double identity = __builtin_huge_val();
   __device__ double operator()(double a, double b) const { return fmin(a, b); }
 };
+// NaN-propagating max / min (np.max / np.min semantics) for the final combine.
+struct PropMaxOp {
+  static constexpr double identity = -__builtin_huge_val();
+  __device__ double operator()(double a, double b) const { return (a != a || b != b) ? a + b : fmax(a, b); }
+};
+struct PropMinOp {
+  static constexpr double identity = __builtin_huge_val();
+  __device__ double operator()(double a, double b) const { return (a != a || b != b) ? a + b : fmin(a, b); }
+};
 
 // Reduce one value per thread to thread 0 of the block.  ``red`` must hold
 // 32 doubles.  Deterministic: the combine order depends only on blockDim.

@@ -62,11 +62,11 @@ __global__ void finish_kernel_kinds(const double* __restrict__ partials, int nbl
   double v = kind == RED_SUM ? 0.0 : (kind == RED_MAX ? -INFINITY : INFINITY);
   for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
     const double x = p[i];
-    v = kind == RED_SUM ? v + x : (kind == RED_MAX ? fmax(v, x) : fmin(v, x));
+    v = kind == RED_SUM ? v + x : (kind == RED_MAX ? PropMaxOp()(v, x) : PropMinOp()(v, x));
   }
   if (kind == RED_SUM) v = block_reduce(v, SumOp(), red);
-  else if (kind == RED_MAX) v = block_reduce(v, MaxOp(), red);
-  else v = block_reduce(v, MinOp(), red);
+  else if (kind == RED_MAX) v = block_reduce(v, PropMaxOp(), red);
+  else v = block_reduce(v, PropMinOp(), red);
   if (threadIdx.x == 0) result[row] = v;
 }
 

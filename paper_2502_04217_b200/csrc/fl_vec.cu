@@ -403,6 +403,35 @@ __global__ void k_ftb(int64_t n, const double* __restrict__ v, const double* __r
   emit(s, NanMinOp(), red, partials, 0);
 }
 
+// np.sign(x) * np.maximum(np.abs(x) - t, 0.0) (diagnostics.py:325-328) with
+// NumPy's conventions: sign(+-0) = +0, sign(NaN) = NaN, maximum(m, 0) = m only
+// when m > 0 or m is NaN (so -0.0 becomes +0.0).
+__device__ __forceinline__ double soft(double x, double t) {
+  const double sg = x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (x == x ? 0.0 : x));
+  const double m = sub(fabs(x), t);
+  return mul(sg, (m > 0.0 || isnan(m)) ? m : 0.0);
+}
+
+__global__ void k_soft(int64_t n, const double* __restrict__ x, double t, double* __restrict__ out) {
+  GRID_LOOP(i, n) out[i] = soft(x[i], t);
+}
+
+// One ISTA iteration (diagnostics.py:352-357) after the gram: grad = G beta - xi,
+// next = soft(beta - grad, lam), step = max |next - beta| (NaN-propagating).
+__global__ void k_ista(int64_t n, const double* __restrict__ beta, const double* __restrict__ gb,
+                       const double* __restrict__ xi, double lam, double* __restrict__ next,
+                       double* __restrict__ partials) {
+  __shared__ double red[32];
+  double s = 0.0;
+  GRID_LOOP(i, n) {
+    const double b = beta[i];
+    const double nx = soft(sub(b, sub(gb[i], xi[i])), lam);
+    next[i] = nx;
+    s = nanmax(s, fabs(sub(nx, b)));
+  }
+  emit(s, NanMaxOp(), red, partials, 0);
+}
+
 __global__ void k_axpy(int64_t n, double alpha, const double* __restrict__ x, double* __restrict__ y) {
   GRID_LOOP(i, n) y[i] = add(y[i], mul(alpha, x[i]));
 }
@@ -981,6 +1010,27 @@ int fl_ftb_ratio(int64_t n, const double* v, const double* dv, double* out, fl_s
   FL_LAUNCH_CHECK();
   const int kind = RED_MIN;
   return reduce_fetch(sc, grid, 1, &kind, out, s);
+}
+
+int fl_soft_threshold(int64_t n, const double* x, double t, double* out, fl_stream_t stream) {
+  if (n < 0 || (n && (!x || !out))) return fail(FL_E_VALUE, "null argument");
+  if (n == 0) return FL_OK;
+  k_soft<<<grid_for(n, T), T, 0, (cudaStream_t)stream>>>(n, x, t, out);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+int fl_ista_step(int64_t n, const double* beta, const double* gram_beta, const double* xi, double lam,
+                 double* next, double* step, fl_stream_t stream) {
+  if (n <= 0 || !beta || !gram_beta || !xi || !next || !step) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  const int grid = grid_for(n, T);
+  k_ista<<<grid, T, 0, s>>>(n, beta, gram_beta, xi, lam, next, sc->partials);
+  FL_LAUNCH_CHECK();
+  const int kind = RED_MAX;
+  return reduce_fetch(sc, grid, 1, &kind, step, s);
 }
 
 int fl_axpy(int64_t n, double alpha, const double* x, double* y, fl_stream_t stream) {

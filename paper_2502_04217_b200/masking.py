@@ -19,7 +19,7 @@ from . import _dev, _lib
 from .errors import UnsupportedShapeError
 from .fourier import GridShape
 
-__all__ = ["Mask", "observe", "observe_adjoint", "gram", "embed"]
+__all__ = ["Mask", "observe", "observe_adjoint", "gram", "embed", "restrict"]
 
 
 class DeviceMask:
@@ -117,6 +117,23 @@ def observe(beta, mask: Mask):
     obs = _dev.empty(mask.n_observed)
     _lib.call("fl_gather_observed", mask.shape.n, _dev.ptr(dm.bits), _dev.ptr(dm.offsets),
               _dev.ptr(x), _dev.ptr(obs), _dev.stream())
+    return _dev.out(obs, host)
+
+
+def restrict(values, mask: Mask):
+    """values[~mask.missing_bool] for a full-grid volume, gathered on the device.
+
+    The CLI's ``b = values[~mask.missing_bool]`` (cli.py:73) without a host
+    pass; NumPy in -> NumPy out, CUDA tensor in -> CUDA tensor out.
+    """
+    host = not _dev.is_device(values)
+    v = _dev.to_dev(values, mask.shape.n, "volume")
+    if mask.n_missing == 0:
+        return _dev.out(v.clone(), host)
+    dm = mask.on_device()
+    obs = _dev.empty(mask.n_observed)
+    _lib.call("fl_gather_observed", mask.shape.n, _dev.ptr(dm.bits), _dev.ptr(dm.offsets),
+              _dev.ptr(v), _dev.ptr(obs), _dev.stream())
     return _dev.out(obs, host)
 
 

@@ -79,3 +79,16 @@ def test_solve_trajectories_match_reference(name):
     assert rep.krylov_counts == [r["krylov_iters"] for r in recs]
     np.testing.assert_allclose(beta, g["beta"], rtol=0, atol=1e-15 * max(1.0, np.abs(g["beta"]).max()))
     assert abs(rep.final_objective - float(g["final_objective"])) <= 1e-14 * abs(float(g["final_objective"]))
+
+
+def test_ista_and_soft_threshold_match_reference():
+    g = load_golden("ista")
+    out = orc.soft_threshold(g["soft_x"], float(g["soft_t"]))
+    assert out.tobytes() == g["soft_out"].tobytes()
+    for name in json.loads(str(g["cases_json"])):
+        m = orc.make_mask(tuple(g[name + "_dims"]), missing=g[name + "_missing"])
+        beta, iters = orc.ista(g[name + "_b"], m, float(g[name + "_lam"]), tol=1e-10)
+        assert iters == int(g[name + "_iters"])
+        np.testing.assert_array_equal(beta, g[name + "_beta"])
+        assert orc.lasso_objective(beta, g[name + "_b"], m, float(g[name + "_lam"])) == \
+            float(g[name + "_objective"])
