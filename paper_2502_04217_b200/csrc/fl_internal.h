@@ -26,6 +26,7 @@ struct fl_plan {
   LongAxis lng[3];
   bool planned[3] = {true, true, true};  // false: batch extent of a slab plan
   std::vector<void*> owned;  // device allocations (twiddle tables)
+  void* pcg_graphs = nullptr;  // cached device-looped PCG graphs (fl_pcg.cu)
 };
 
 namespace fl {
@@ -82,8 +83,13 @@ int pcg2_init(int64_t n, const double* sig1, const double* sig2, const double* r
 int pcg2_update(int64_t n, const double* sig1, const double* sig2, const double* rho, const double* curv_g,
                 const double* curv_d, double* x, double* r, const double* p, const double* gp,
                 double* partials, int* nblocks, cudaStream_t s);
+// beta_dev (optional) overrides beta on the device; done (optional) makes the
+// kernel a no-op once the device-looped PCG has stopped.
 int pcg2_pupdate(int64_t n, const double* sig1, const double* sig2, const double* r, double beta, double* p,
-                 double* partials, int* nblocks, cudaStream_t s);
+                 double* partials, int* nblocks, cudaStream_t s, const double* beta_dev = nullptr,
+                 const int* done = nullptr);
+// Release the plan's cached PCG graphs (fl_plan_destroy).
+void pcg_graphs_release(fl_plan* p);
 int dot_partials(int64_t n, const double* a, const double* b, double* partials, int* nblocks, cudaStream_t s);
 
 }  // namespace fl

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "fl_common.cuh"
 #include "fl_internal.h"
@@ -121,6 +122,197 @@ int pcg_v2(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double
 }
 
 
+// ---------------------------------------------------------------------------
+// v3 (default when no host history is requested): the v2 iteration captured
+// once per (plan, operands) into a CUDA graph whose WHILE conditional node
+// loops on the device.  A one-thread control kernel after the update pass
+// performs pcg.py's scalar step (breakdown checks, the stopping test, beta)
+// and clears the loop condition, so a whole PCG solve is ONE graph launch and
+// ONE host sync instead of one sync per iteration.  Same kernels, same
+// operands, same scalar arithmetic (IEEE sqrt / divide) as v2.
+// ---------------------------------------------------------------------------
+
+struct PcgCtl {      // at work + 6n + 8 (8 doubles)
+  double thr;        // stopping threshold abs_tol + rel_tol * ||r0||_P
+  double norm;       // last preconditioned residual norm
+  double bad;        // offending value of a breakdown
+  long long limit;   // iteration cap
+  long long k;       // iterations done
+  int status;        // 0 running, 1 converged, 2 cap reached, 3 curvature, 4 r'P^{-1}r breakdown
+  int done;
+};
+static_assert(sizeof(PcgCtl) <= 8 * sizeof(double), "PcgCtl must fit its work slots");
+
+// slots: [rho, rho_next, curv_G, curv_diag, beta]
+__global__ void k_pcg_control(PcgCtl* __restrict__ c, double* __restrict__ slots,
+                              cudaGraphConditionalHandle h) {
+  if (threadIdx.x != 0) return;
+  if (c->done) {
+    cudaGraphSetConditional(h, 0);
+    return;
+  }
+  const long long k = ++c->k;
+  const double curv = slots[2] + slots[3];
+  const double rn = slots[1];
+  int st = 0;
+  double bad = 0.0;
+  if (!isfinite(curv) || curv <= 0) {
+    st = 3;
+    bad = curv;
+  } else if (!isfinite(rn) || rn < 0) {
+    st = 4;
+    bad = rn;
+  } else {
+    const double norm = sqrt(rn);
+    c->norm = norm;
+    if (norm <= c->thr) {
+      st = 1;
+    } else if (k >= c->limit) {
+      st = 2;
+    } else {
+      slots[4] = rn / slots[0];  // beta = rz_new / rz (pcg.py)
+      slots[0] = rn;
+    }
+  }
+  if (st) {
+    c->status = st;
+    c->bad = bad;
+    c->done = 1;
+    cudaGraphSetConditional(h, 0);
+  }
+}
+
+struct PcgGraph {
+  const uint32_t* bits;
+  const double *sig1, *sig2;
+  double *x, *work;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+struct PcgGraphs {
+  std::vector<PcgGraph> v;
+  cudaStream_t capture = nullptr;
+};
+
+// Enqueue one v2 iteration with device-side scalars (captured into the body).
+int enqueue_iteration(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, double* x,
+                      double* work, cudaGraphConditionalHandle h, cudaStream_t s) {
+  const int64_t n = p->n;
+  double* r = work;
+  double* pv = work + 2 * n;
+  double* gp = work + 4 * n;
+  double* slots = work + 6 * n;
+  PcgCtl* ctl = reinterpret_cast<PcgCtl*>(slots + 8);
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  const int ksum = RED_SUM;
+  int nbg = 0, nbu = 0, nbp = 0;
+  bool have_norm = false;
+  FL_TRY(op_gram_norm(p, bits, pv, gp, sc->partials, &nbg, &have_norm, s));
+  if (!have_norm) FL_TRY(dot_partials(n, pv, gp, sc->partials, &nbg, s));
+  FL_TRY(finish_reduce(sc->partials, nbg, 1, &ksum, slots + 2, s));
+  FL_TRY(pcg2_update(n, sigma1, sigma2, slots, slots + 2, slots + 3, x, r, pv, gp, sc->partials, &nbu, s));
+  FL_TRY(finish_reduce(sc->partials, nbu, 1, &ksum, slots + 1, s));
+  k_pcg_control<<<1, 32, 0, s>>>(ctl, slots, h);
+  FL_LAUNCH_CHECK();
+  FL_TRY(pcg2_pupdate(n, sigma1, sigma2, r, 0.0, pv, sc->partials, &nbp, s, slots + 4, &ctl->done));
+  FL_TRY(finish_reduce(sc->partials, nbp, 1, &ksum, slots + 3, s));
+  return FL_OK;
+}
+
+int pcg_graph(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, double* x,
+              double* work, cudaGraphExec_t* out) {
+  auto* gs = static_cast<PcgGraphs*>(p->pcg_graphs);
+  if (!gs) {
+    gs = new PcgGraphs();
+    p->pcg_graphs = gs;
+  }
+  for (const PcgGraph& g : gs->v)
+    if (g.bits == bits && g.sig1 == sigma1 && g.sig2 == sigma2 && g.x == x && g.work == work) {
+      *out = g.exec;
+      return FL_OK;
+    }
+  if (!gs->capture) FL_CUDA(cudaStreamCreateWithFlags(&gs->capture, cudaStreamNonBlocking));
+  PcgGraph g{bits, sigma1, sigma2, x, work};
+  FL_CUDA(cudaGraphCreate(&g.graph, 0));
+  cudaGraphConditionalHandle h;
+  FL_CUDA(cudaGraphConditionalHandleCreate(&h, g.graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  FL_CUDA(cudaGraphAddNode(&node, g.graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  FL_CUDA(cudaStreamBeginCaptureToGraph(gs->capture, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  const int st = enqueue_iteration(p, bits, sigma1, sigma2, x, work, h, gs->capture);
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(gs->capture, &captured);
+  if (st != FL_OK || ce != cudaSuccess) {
+    cudaGraphDestroy(g.graph);
+    return st != FL_OK ? st : fail(FL_E_CUDA, std::string("PCG graph capture: ") + cudaGetErrorString(ce));
+  }
+  const cudaError_t ie = cudaGraphInstantiate(&g.exec, g.graph, 0);
+  if (ie != cudaSuccess) {
+    cudaGraphDestroy(g.graph);
+    return fail(FL_E_CUDA, std::string("PCG graph instantiate: ") + cudaGetErrorString(ie));
+  }
+  gs->v.push_back(g);
+  *out = g.exec;
+  return FL_OK;
+}
+
+int pcg_v3(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, const double* rhs,
+           double* x, double* work, double abs_tol, double rel_tol, int64_t max_iters, fl_pcg_result* res,
+           cudaStream_t s) {
+  const int64_t n = p->n;
+  double* r = work;
+  double* pv = work + 2 * n;
+  double* slots = work + 6 * n;
+  PcgCtl* ctl = reinterpret_cast<PcgCtl*>(slots + 8);
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  const int64_t limit = max_iters >= 0 ? max_iters : std::min<int64_t>(10 * 2 * n, kPcgIterCap);
+  const int sum2[2] = {RED_SUM, RED_SUM};
+  int nb = 0;
+  FL_TRY(pcg2_init(n, sigma1, sigma2, rhs, x, r, pv, sc->partials, &nb, s));
+  FL_TRY(finish_reduce(sc->partials, nb, 2, sum2, sc->result, s));
+  FL_CUDA(cudaMemcpyAsync(slots, sc->result, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  FL_CUDA(cudaMemcpyAsync(slots + 3, sc->result + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  FL_CUDA(cudaMemcpyAsync(sc->host, slots, sizeof(double), cudaMemcpyDeviceToHost, s));
+  FL_CUDA(cudaStreamSynchronize(s));
+  const double rho = sc->host[0];
+  FL_TRY(check_rho(rho, 0));
+  const double norm0 = std::sqrt(rho);
+  const double thr = abs_tol + rel_tol * norm0;
+  res->norm0 = norm0;
+  if (norm0 <= thr || limit <= 0) {
+    res->iterations = 0;
+    res->converged = norm0 <= thr;
+    res->residual_norm = norm0;
+    return FL_OK;
+  }
+  cudaGraphExec_t exec;
+  FL_TRY(pcg_graph(p, bits, sigma1, sigma2, x, work, &exec));
+  PcgCtl* hc = reinterpret_cast<PcgCtl*>(sc->host);
+  *hc = PcgCtl{thr, norm0, 0.0, (long long)limit, 0, 0, 0};
+  FL_CUDA(cudaMemcpyAsync(ctl, hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
+  FL_CUDA(cudaGraphLaunch(exec, s));
+  FL_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, s));
+  FL_CUDA(cudaStreamSynchronize(s));
+  const PcgCtl c = *hc;
+  if (c.status == 3) return check_curv(c.bad, c.k);
+  if (c.status == 4) return check_rho(c.bad, c.k);
+  if (c.status != 1 && c.status != 2) return fail(FL_E_CUDA, "device PCG loop ended without a verdict");
+  res->iterations = c.k;
+  res->converged = c.status == 1;
+  res->residual_norm = c.norm;
+  return FL_OK;
+}
+
+
 // v1: materialised K p (gram + elementwise epilogue with d.Kd partials), then
 // a fused update pass reading K p; kept behind FL_PCG_V1=1 for comparison.
 int pcg_v1(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, const double* rhs,
@@ -194,6 +386,20 @@ int pcg_v1(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double
 
 }  // namespace
 
+namespace fl {
+void pcg_graphs_release(fl_plan* p) {
+  auto* gs = static_cast<PcgGraphs*>(p->pcg_graphs);
+  if (!gs) return;
+  for (PcgGraph& g : gs->v) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+  }
+  if (gs->capture) cudaStreamDestroy(gs->capture);
+  delete gs;
+  p->pcg_graphs = nullptr;
+}
+}  // namespace fl
+
 extern "C" {
 
 int64_t fl_pcg_work_doubles(int64_t n) { return 6 * n + 16; }
@@ -206,11 +412,15 @@ int fl_pcg_kkt(fl_plan_t p, const uint32_t* bits, const double* sigma1, const do
     return fail(FL_E_VALUE, "null argument");
   if (abs_tol < 0 || rel_tol < 0) return fail(FL_E_VALUE, "tolerances must be nonnegative");
   if (abs_tol == 0 && rel_tol == 0) return fail(FL_E_VALUE, "abs_tol and rel_tol cannot both be zero");
-  static const bool v1 = [] {
-    const char* e = std::getenv("FL_PCG_V1");
-    return e && e[0] == '1';
+  static const int mode = [] {
+    const char* e = std::getenv("FL_PCG");  // 1: v1, 2: v2 (host loop), default 3 (graph loop)
+    const char* v1 = std::getenv("FL_PCG_V1");
+    if (v1 && v1[0] == '1') return 1;
+    return e ? std::atoi(e) : 3;
   }();
-  auto* run = v1 ? pcg_v1 : pcg_v2;
+  if (mode == 3 && !(history && max_history > 0) && p->n % 2 == 0)
+    return pcg_v3(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, max_iters, res, (cudaStream_t)stream);
+  auto* run = mode == 1 ? pcg_v1 : pcg_v2;
   return run(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, max_iters, res, history, max_history,
              (cudaStream_t)stream);
 }

@@ -201,6 +201,7 @@ int fl_plan_create_ex(int ndim, const int64_t* dims, int transform_axes, int dev
 
 int fl_plan_destroy(fl_plan_t p) {
   if (!p) return FL_OK;
+  pcg_graphs_release(p);
   for (void* d : p->owned) cudaFree(d);
   delete p;
   return FL_OK;

@@ -602,8 +602,11 @@ __global__ void k_pcg2_update(int64_t n, const double* __restrict__ g1, const do
 
 __global__ void k_pcg2_pupdate(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
                                const double* __restrict__ r, double beta, double* __restrict__ p,
-                               double* __restrict__ partials) {
+                               double* __restrict__ partials, const double* __restrict__ beta_dev,
+                               const int* __restrict__ done) {
   __shared__ double red[32];
+  if (done && *done) return;
+  if (beta_dev) beta = *beta_dev;
   double dq = 0.0;
   const int64_t n2 = n >> 1;
   const double2* G1 = reinterpret_cast<const double2*>(g1);
@@ -737,10 +740,10 @@ int pcg2_update(int64_t n, const double* sig1, const double* sig2, const double*
 }
 
 int pcg2_pupdate(int64_t n, const double* sig1, const double* sig2, const double* r, double beta, double* p,
-                 double* partials, int* nblocks, cudaStream_t s) {
+                 double* partials, int* nblocks, cudaStream_t s, const double* beta_dev, const int* done) {
   if (n % 2) return fail(FL_E_SHAPE, "PCG p-update needs an even length (16-byte accesses)");
   const int grid = grid_for(n, T);
-  k_pcg2_pupdate<<<grid, T, 0, s>>>(n, sig1, sig2, r, beta, p, partials);
+  k_pcg2_pupdate<<<grid, T, 0, s>>>(n, sig1, sig2, r, beta, p, partials, beta_dev, done);
   FL_LAUNCH_CHECK();
   *nblocks = grid;
   return FL_OK;

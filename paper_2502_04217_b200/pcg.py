@@ -9,8 +9,9 @@ Two entry points:
   return NumPy arrays (drop-in for the reference's callers); with a CUDA
   tensor they receive CUDA tensors.
 * ``kkt_pcg(...)`` -- the solver's hot loop: PCG on the condensed KKT system
-  fully inside the C library (``fl_pcg_kkt``), fused matvec + fused update,
-  one host round trip per iteration.
+  fully inside the C library (``fl_pcg_kkt``), fused matvec + fused update;
+  the iteration loop runs on the device (a CUDA graph with a WHILE node), so a
+  whole PCG solve is one graph launch and one host round trip.
 """
 
 from __future__ import annotations

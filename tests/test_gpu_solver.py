@@ -253,3 +253,67 @@ print(json.dumps(out))
         assert all(abs(a - b) <= 1 for a, b in zip(k0, k1))
         assert abs(o0 - o1) <= 1e-9 * abs(o1)
         assert np.allclose(b0, b1, atol=1e-7)
+
+
+def test_pcg_graph_loop_bitwise_equals_host_loop():
+    """FL_PCG=3 (default: one CUDA graph with a device WHILE loop per PCG
+    solve) runs the same kernels and scalar recurrences as FL_PCG=2 (host
+    loop, one sync per iteration): identical Krylov counts and bitwise
+    identical solutions."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    code = r'''
+import sys, json, hashlib, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_2502_04217_b200 as fl
+from conftest import load_golden
+out = {}
+for name in ("c1_4096", "c2_256", "c3_32", "harm_16", "empty_128", "maxit_64"):
+    g = load_golden("solve_" + name)
+    dims = tuple(int(d) for d in g["dims"])
+    mi = 3 if name == "maxit_64" else 200
+    lam = float(g["lam"])
+    beta, rep = fl.solve(g["b"], fl.Mask(g["missing"], fl.GridShape(dims)), fl.IpmConfig(lam=lam, max_iters=mi))
+    out[name] = [rep.krylov_counts, [r.pcg_residual for r in rep.records], hashlib.sha1(beta.tobytes()).hexdigest()]
+print(json.dumps(out))
+''' % (REPO, REPO + "/tests")
+    res = {}
+    for mode in ("2", "3"):
+        env = dict(os.environ, FL_PCG=mode)
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[mode] = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["2"] == res["3"]
+
+
+def test_pcg_graph_loop_breakdown_and_cap():
+    """Device-loop verdicts map to the host-loop errors: nonpositive curvature
+    raises NumericalBreakdownError; the iteration cap returns not-converged."""
+    from paper_2502_04217_b200 import _dev
+    import torch
+
+    n = 64
+    shape = fl.GridShape((n,))
+    mask = fl.Mask(np.arange(0, n, 2), shape)  # half the samples missing
+    dm = mask.on_device()
+    plan = _dev.plan_for(shape.dims)
+    rng = np.random.default_rng(5)
+    rhs = torch.from_numpy(rng.standard_normal(2 * n)).cuda()
+    x = _dev.empty(2 * n)
+    work = _dev.empty(fl._lib.lib().fl_pcg_work_doubles(n))
+    from paper_2502_04217_b200.pcg import kkt_pcg
+    # sigma = (0.55, -0.05): Lambda1 = 0.5, Lambda2 = 0.6, so P (I + Lambda1 in
+    # the top block) is positive definite (r'P^{-1}r > 0) while K is
+    # indefinite on the missing samples -> nonpositive curvature inside the loop
+    s1 = torch.full((n,), 0.55, dtype=torch.float64, device="cuda")
+    s2 = torch.full((n,), -0.05, dtype=torch.float64, device="cuda")
+    with pytest.raises(fl.NumericalBreakdownError, match="curvature"):
+        kkt_pcg(plan, dm, s1, s2, rhs, x, work, PcgConfig(abs_tol=1e-12))
+    s1 = torch.from_numpy(np.abs(rng.standard_normal(n)) + 0.1).cuda()
+    s2 = torch.from_numpy(np.abs(rng.standard_normal(n)) + 0.1).cuda()
+    res = kkt_pcg(plan, dm, s1, s2, rhs, x, work, PcgConfig(abs_tol=1e-30, max_iters=2))
+    assert res.iterations == 2 and not res.converged
