@@ -104,13 +104,37 @@ __device__ __forceinline__ void issue_tile(const PassArgs& A, int64_t tile, doub
 #pragma unroll
   for (int r = 0; r < G::E; ++r) {
     const int k = q + r * G::P;
-    double2* dst = st + stage_idx<M, STRIDED, CFG>(k, c);
     if (STRIDED) {
-      cp_async16(dst, A.in + Q.bx + k * Q.st);
+      cp_async16(st + stage_idx<M, STRIDED, CFG>(k, c), A.in + Q.bx + k * Q.st);
     } else {
-      cp_async8(&dst->x, A.in + Q.bx + k);
-      if (Q.by >= 0) cp_async8(&dst->y, A.in + Q.by + k);
+      // planar rows (x row then y row of the pair): conflict-free 8-byte fills
+      double* row = reinterpret_cast<double*>(st) + 2 * c * M;
+      cp_async8(row + k, A.in + Q.bx + k);
+      if (Q.by >= 0) cp_async8(row + M + k, A.in + Q.by + k);
     }
+  }
+}
+
+// Contiguous axis: the tile's W row pairs as 2W TMA bulk copies (4 KiB rows at
+// m = 512) into the planar stage, issued by one thread, completing on ``bar``.
+template <int M, int CFG>
+__device__ __forceinline__ void tma_tile(const PassArgs& A, int64_t tile, double2* st, unsigned long long* bar) {
+  using G = Geom<M, CFG>;
+  unsigned bytes = 0;
+#pragma unroll 1
+  for (int c = 0; c < G::W; ++c) {
+    const int64_t g = tile * G::W + c;
+    if (g < A.G) bytes += (geo<false>(A, g).by >= 0 ? 2u : 1u) * M * 8u;
+  }
+  fast::mbar_expect_tx(bar, bytes);
+#pragma unroll 1
+  for (int c = 0; c < G::W; ++c) {
+    const int64_t g = tile * G::W + c;
+    if (g >= A.G) break;
+    const Geo Q = geo<false>(A, g);
+    double* row = reinterpret_cast<double*>(st) + 2 * c * M;
+    fast::bulk_g2s(row, A.in + Q.bx, M * 8u, bar);
+    if (Q.by >= 0) fast::bulk_g2s(row + M, A.in + Q.by, M * 8u, bar);
   }
 }
 
@@ -121,8 +145,13 @@ __device__ __forceinline__ double2 raw(const PassArgs& A, const double2* st, con
   double2 z = make_double2(0.0, 0.0);
   if (!valid) return z;
   if (PIPE) {
-    z = st[stage_idx<M, STRIDED, CFG>(k, c)];
-    if (!STRIDED && Q.by < 0) z.y = 0.0;
+    if (STRIDED) {
+      z = st[stage_idx<M, STRIDED, CFG>(k, c)];
+    } else {
+      const double* row = reinterpret_cast<const double*>(st) + 2 * c * M;
+      z.x = row[k];
+      z.y = Q.by < 0 ? 0.0 : row[M + k];
+    }
   } else if (STRIDED) {
     z = *reinterpret_cast<const double2*>(A.in + Q.bx + (int64_t)k * Q.st);
   } else {
@@ -136,9 +165,13 @@ __device__ __forceinline__ double2 raw(const PassArgs& A, const double2* st, con
 // the stage, start copying the next tile into it (overlaps this tile's FFT).
 template <int M, bool STRIDED, int CFG>
 __device__ __forceinline__ void refill(const PassArgs& A, int64_t next, int64_t ntiles, double2* stage,
-                                       int c, int q) {
+                                       int c, int q, unsigned long long* bar = nullptr) {
   if constexpr (Geom<M, CFG>::PIPE == 1) {
     __syncthreads();
+    if (bar) {
+      if (threadIdx.x == 0 && next < ntiles) tma_tile<M, CFG>(A, next, stage, bar);
+      return;
+    }
     if (next < ntiles) issue_tile<M, STRIDED, CFG>(A, next, stage, c, q);
     cp_commit();
   }
@@ -163,9 +196,25 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
   const double c0 = A.c0, c1 = A.c1;
   double acc = 0.0, nrm = 0.0;
   const int64_t ntiles = (A.G + W - 1) / W;
+  // contiguous rows with single staging: TMA bulk row copies on an mbarrier
+  // (one issuing thread, no per-thread cp.async, conflict-free planar fills)
+  __shared__ unsigned long long tbar;
+  unsigned long long* bar = nullptr;
+  unsigned tphase = 0;
+  if constexpr (!STRIDED && PIPE == 1) {
+    if ((reinterpret_cast<uintptr_t>(A.in) & 15) == 0) {
+      bar = &tbar;
+      if (threadIdx.x == 0) fast::mbar_init(bar, 1);
+      __syncthreads();
+    }
+  }
   if (PIPE > 0) {
-    if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, CFG>(A, blockIdx.x, stage0, c, q);
-    cp_commit();
+    if (bar) {
+      if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntiles) tma_tile<M, CFG>(A, blockIdx.x, stage0, bar);
+    } else {
+      if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, CFG>(A, blockIdx.x, stage0, c, q);
+      cp_commit();
+    }
   }
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -180,8 +229,13 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
       cp_wait<1>();
       __syncthreads();
     } else if (PIPE == 1) {
-      cp_wait<0>();
-      __syncthreads();
+      if (bar) {
+        fast::mbar_wait(bar, tphase);
+        tphase ^= 1u;
+      } else {
+        cp_wait<0>();
+        __syncthreads();
+      }
     }
     double2 v[E];
     if constexpr (KIND == K_COPY) {
@@ -212,7 +266,7 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
       if (PIPE > 0) {
 #pragma unroll
         for (int r = 0; r < E; ++r) v[r] = raw<M, STRIDED, (PIPE > 0), CFG>(A, st, Q, valid, q + r * P, c);
-        refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
+        refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q, bar);
       } else {
         // base pointer of row q, rows advance by P*st (no per-element 64-bit multiplies)
         const double* px = A.in + Q.bx + (int64_t)q * Q.st;
@@ -262,7 +316,7 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
           }
           v[r] = z;
         }
-        refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
+        refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q, bar);
       } else {
         // unpack packed rows (j+1, j+h) into the combined half spectra Zin_j, Zin_{M-j}
         const int qm = -q + ((-q) >> 3);
