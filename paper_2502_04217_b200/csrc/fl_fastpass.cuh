@@ -525,52 +525,41 @@ __global__ void __launch_bounds__(mirror::MGeom<M>::T, MB) mirror_pass(const Pas
     } else {
       // Zin_j and Zin_{M-j} from ONE read of the packed rows (j+1, j+H) of
       // j = min(k, M-k); the two values land in the mirror slot pair.
-      auto rows = [&](int j, double2& a, double2& bb) {
-        a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + 1, c);
-        bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, j + H, c);
-      };
       auto lo = [&](const double2& a, const double2& bb) {  // Zin_j
         return make_double2(c1 * (a.x - bb.y), c1 * (bb.x + a.y));
       };
       auto hi = [&](const double2& a, const double2& bb) {  // Zin_{M-j}
         return make_double2(c1 * (a.x + bb.y), c1 * (a.y - bb.x));
       };
-      if (!q0) {
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          // pair: slot (0, s) holds k0 = q + s NB, slot (1, 7-s) holds M - k0
-          const int j = s < 4 ? mirror::slot_k<M>(q, 0, s) : mirror::slot_k<M>(q, 1, 7 - s);
-          double2 a, bb;
-          rows(j, a, bb);
-          if (s < 4) {
-            v[s] = lo(a, bb);
-            v[8 + 7 - s] = hi(a, bb);
-          } else {
-            v[8 + 7 - s] = lo(a, bb);
-            v[s] = hi(a, bb);
-          }
+      // Eight row-pair reads per thread, the same code for every lane (a
+      // branch on q == 0 would serialise that warp's loads): q = 0 owns the
+      // self-mirrored butterflies 0 and NB/2, handled by index / value
+      // selects -- rows (0, 1) hold Z_0, Z_H unscaled-paired, its b = 1
+      // butterfly starts at NB/2, and its hi values land in other slots.
+      constexpr int NB = G::NB;
+      const int jb1 = q0 ? NB / 2 : NB - q;
+      // hi value i goes to slot GEN[i] (q != 0) or Q0[i] (q == 0); both maps
+      // are permutations of the same 8 slots, so two selects per value keep
+      // nothing extra live: each slot is written once under either regime.
+      constexpr int GEN[8] = {15, 14, 13, 12, 4, 5, 6, 7};
+      constexpr int Q0[8] = {4, 7, 6, 5, 12, 13, 14, 15};
+      fast::static_for<0, 8>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const int j = i < 4 ? q + i * NB : jb1 + (7 - i) * NB;
+        const bool sp = i == 0 && q0;
+        double2 a, bb;
+        a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, sp ? 0 : j + 1, c);
+        bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, sp ? 1 : j + H, c);
+        double2 l = lo(a, bb), h = hi(a, bb);
+        if constexpr (i == 0) {
+          l = sp ? make_double2(c0 * a.x, c0 * a.y) : l;
+          h = sp ? make_double2(c0 * bb.x, c0 * bb.y) : h;
         }
-      } else {
-        // q == 0: butterflies 0 and NB/2 are self-mirrored
-        const double2 r0 = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 0, c);
-        const double2 r1 = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, 1, c);
-        v[0] = make_double2(c0 * r0.x, c0 * r0.y);
-        v[4] = make_double2(c0 * r1.x, c0 * r1.y);
-#pragma unroll
-        for (int s = 1; s < 4; ++s) {
-          double2 a, bb;
-          rows(mirror::slot_k<M>(0, 0, s), a, bb);
-          v[s] = lo(a, bb);
-          v[8 - s] = hi(a, bb);
-        }
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          double2 a, bb;
-          rows(mirror::slot_k<M>(0, 1, s), a, bb);
-          v[8 + s] = lo(a, bb);
-          v[8 + 7 - s] = hi(a, bb);
-        }
-      }
+        if constexpr (i < 4) v[i] = l;
+        else v[15 - i] = l;
+        v[GEN[i]] = q0 ? v[GEN[i]] : h;
+        v[Q0[i]] = q0 ? h : v[Q0[i]];
+      });
     }
     refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
     // mask bits of the 16 slots (x: bit 2i, y: bit 2i+1) packed into one
