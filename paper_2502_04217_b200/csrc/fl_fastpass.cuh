@@ -118,7 +118,9 @@ __device__ __forceinline__ void issue_tile(const PassArgs& A, int64_t tile, doub
 // Contiguous axis: the tile's W row pairs as 2W TMA bulk copies (4 KiB rows at
 // m = 512) into the planar stage, issued by one thread, completing on ``bar``.
 template <int M, int CFG>
-__device__ __forceinline__ void tma_tile(const PassArgs& A, int64_t tile, double2* st, unsigned long long* bar) {
+__device__ __forceinline__ void tma_tile(const PassArgs& A, int64_t tile, double2* st, unsigned long long* bar,
+                                         const double* src = nullptr) {
+  if (!src) src = A.in;
   using G = Geom<M, CFG>;
   unsigned bytes = 0;
 #pragma unroll 1
@@ -133,8 +135,8 @@ __device__ __forceinline__ void tma_tile(const PassArgs& A, int64_t tile, double
     if (g >= A.G) break;
     const Geo Q = geo<false>(A, g);
     double* row = reinterpret_cast<double*>(st) + 2 * c * M;
-    fast::bulk_g2s(row, A.in + Q.bx, M * 8u, bar);
-    if (Q.by >= 0) fast::bulk_g2s(row + M, A.in + Q.by, M * 8u, bar);
+    fast::bulk_g2s(row, src + Q.bx, M * 8u, bar);
+    if (Q.by >= 0) fast::bulk_g2s(row + M, src + Q.by, M * 8u, bar);
   }
 }
 
@@ -198,13 +200,21 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
   const int64_t ntiles = (A.G + W - 1) / W;
   // contiguous rows with single staging: TMA bulk row copies on an mbarrier
   // (one issuing thread, no per-thread cp.async, conflict-free planar fills)
-  __shared__ unsigned long long tbar;
+  // The residual pass (K_RESID) also stages its b_hat rows: issued at the top
+  // of each tile on a second barrier into a second planar stage, consumed
+  // after the inverse FFT (the loads no longer wait behind it).
+  __shared__ unsigned long long tbar[2];
   unsigned long long* bar = nullptr;
-  unsigned tphase = 0;
+  unsigned tphase = 0, bphase = 0;
+  constexpr bool BSTAGE = KIND == K_RESID && !STRIDED && PIPE == 1;
+  const double* bstage = reinterpret_cast<const double*>(stage0 + W * M);
   if constexpr (!STRIDED && PIPE == 1) {
-    if ((reinterpret_cast<uintptr_t>(A.in) & 15) == 0) {
-      bar = &tbar;
-      if (threadIdx.x == 0) fast::mbar_init(bar, 1);
+    if ((reinterpret_cast<uintptr_t>(A.in) & 15) == 0 && (!BSTAGE || (reinterpret_cast<uintptr_t>(A.bhat) & 15) == 0)) {
+      bar = tbar;
+      if (threadIdx.x == 0) {
+        fast::mbar_init(bar, 1);
+        if (BSTAGE) fast::mbar_init(bar + 1, 1);
+      }
       __syncthreads();
     }
   }
@@ -223,6 +233,8 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
     const Geo Q = geo<STRIDED>(A, valid ? g : 0);
     const int64_t next = tile + gridDim.x;
     const double2* st = (PIPE == 2 && (it & 1)) ? stage1 : stage0;
+    if (BSTAGE && bar && threadIdx.x == 0)  // previous tile's b_hat reads ended at its last barrier
+      tma_tile<M, CFG>(A, tile, stage0 + W * M, bar + 1, A.bhat);
     if (PIPE == 2) {
       if (next < ntiles) issue_tile<M, STRIDED, CFG>(A, next, (it & 1) ? stage0 : stage1, c, q);
       cp_commit();
@@ -368,6 +380,11 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
         }
       } else {
         // Z (b_hat - x) or Z x on the synthesized samples, in registers
+        if (BSTAGE && bar) {
+          fast::mbar_wait(bar + 1, bphase);
+          bphase ^= 1u;
+        }
+        const double* brow = bstage + 2 * c * M;
 #pragma unroll
         for (int r = 0; r < E; ++r) {
           const int t = q + r * P;
@@ -375,12 +392,12 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
           if (valid) {
             const int64_t vx = Q.bx + t;
             const bool mx = (wx[r] >> (vx & 31)) & 1u;
-            if (KIND == K_RESID) z.x = mx ? 0.0 : A.bhat[vx] - z.x;
+            if (KIND == K_RESID) z.x = mx ? 0.0 : ((BSTAGE && bar) ? brow[t] : A.bhat[vx]) - z.x;
             else if (mx) z.x = 0.0;
             if (Q.by >= 0) {
               const int64_t vy = Q.by + t;
               const bool my = (wy[r] >> (vy & 31)) & 1u;
-              if (KIND == K_RESID) z.y = my ? 0.0 : A.bhat[vy] - z.y;
+              if (KIND == K_RESID) z.y = my ? 0.0 : ((BSTAGE && bar) ? brow[M + t] : A.bhat[vy]) - z.y;
               else if (my) z.y = 0.0;
             } else {
               z.y = 0.0;
@@ -724,7 +741,7 @@ Entry make_cfg(int kind, bool epi) {
       break;
   }
   e.threads = G::T;
-  e.smem = G::SMEM;
+  e.smem = G::SMEM + ((kind == K_RESID && !S && G::PIPE == 1) ? G::STAGE_BYTES : 0);
   e.w = G::W;
   return e;
 }
