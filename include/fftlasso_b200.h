@@ -290,6 +290,18 @@ FL_API int fl_axpy(int64_t n, double alpha, const double* x, double* y, fl_strea
 /* y = x + beta * y    (NumPy ``p = z + beta * p``) */
 FL_API int fl_xpby(int64_t n, const double* x, double beta, double* y, fl_stream_t stream);
 
+/* ---- fused Newton step front half (ipm.py:303-332) ---------------------
+ * One pass computes the barrier diagonals sigma = nu/s with the interior
+ * check (newton_system.py:72-91 -> FL_E_INTERIOR), the condensed RHS
+ * (newton_system.py:113-145, never stored) and the PCG start, then runs the
+ * condensed PCG (pcg.py:57-127) to x = (d_beta, d_z).  Bitwise equal to
+ * fl_barrier_diagonals + fl_newton_rhs + fl_pcg_kkt; ``sigma1``/``sigma2`` are
+ * written for the back-substitution.  ``work`` as for fl_pcg_kkt. */
+FL_API int fl_ipm_newton_pcg(fl_plan_t plan, const uint32_t* miss_bits, const fl_state* st, const double* g,
+                             double lam, double mu, double* sigma1, double* sigma2, double* x, double* work,
+                             double abs_tol, double rel_tol, int64_t max_iters, fl_pcg_result* res,
+                             fl_stream_t stream);
+
 /* ---- diagnostics (diagnostics.py) -------------------------------------- */
 /* out = sign(x) * max(|x| - t, 0) elementwise, NumPy conventions
  * (soft_threshold, diagnostics.py:325-328); in place allowed. */

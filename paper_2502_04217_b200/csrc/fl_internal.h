@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "fl_fft.cuh"
+#include "fftlasso_b200.h"
 
 // Four-step decomposition of an axis too long for one CTA's shared memory.
 struct LongAxis {
@@ -91,5 +92,8 @@ int pcg2_pupdate(int64_t n, const double* sig1, const double* sig2, const double
 // Release the plan's cached PCG graphs (fl_plan_destroy).
 void pcg_graphs_release(fl_plan* p);
 int dot_partials(int64_t n, const double* a, const double* b, double* partials, int* nblocks, cudaStream_t s);
+// Fused barrier diagonals + condensed RHS + PCG start (rows: rho, diag curvature, interior flag).
+int newton_setup(int64_t n, const fl_state* st, const double* g, double lam, double mu, double* sig1,
+                 double* sig2, double* x, double* r, double* p, double* partials, int* nblocks, cudaStream_t s);
 
 }  // namespace fl

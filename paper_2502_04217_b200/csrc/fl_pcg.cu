@@ -51,9 +51,27 @@ int check_curv(double curv, int64_t k) {
 // reads g = G p_beta and forms K p in registers, so K p never touches HBM.
 // Per iteration: 2d-1 transform passes + update (104 B/voxel) + p-update
 // (64 B/voxel) = 248 B/voxel in 3D, vs 280 for v1.
-int pcg_v2(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, const double* rhs,
-           double* x, double* work, double abs_tol, double rel_tol, int64_t max_iters, fl_pcg_result* res,
-           double* history, int64_t max_history, cudaStream_t s) {
+// Reduce the start partials (rows: rho, diagonal curvature[, interior flag])
+// into slots[0] / slots[3] and read rho (and the flag) back: the one host sync
+// before the loop.
+int pcg_start_fetch(Scratch* sc, int nb, bool with_flag, double* slots, double* rho, double* flag,
+                    cudaStream_t s) {
+  const int kinds[3] = {RED_SUM, RED_SUM, RED_MAX};
+  FL_TRY(finish_reduce(sc->partials, nb, with_flag ? 3 : 2, kinds, sc->result, s));
+  FL_CUDA(cudaMemcpyAsync(slots, sc->result, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  FL_CUDA(cudaMemcpyAsync(slots + 3, sc->result + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  FL_CUDA(cudaMemcpyAsync(sc->host, sc->result, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FL_CUDA(cudaStreamSynchronize(s));
+  *rho = sc->host[0];
+  if (flag) *flag = with_flag ? sc->host[2] : 0.0;
+  return FL_OK;
+}
+
+// v2 loop from a started state (x = 0, r = rhs, p = P^{-1} r; slots[0] = rho,
+// slots[3] = diagonal curvature).
+int pcg_v2_loop(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, double* x,
+                double* work, double rho, double abs_tol, double rel_tol, int64_t limit, fl_pcg_result* res,
+                double* history, int64_t max_history, cudaStream_t s) {
   const int64_t n = p->n;
   double* r = work;
   double* pv = work + 2 * n;
@@ -61,18 +79,7 @@ int pcg_v2(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double
   double* slots = work + 6 * n;  // [rho_a, rho_b, curv_G, curv_diag]
   Scratch* sc;
   FL_TRY(scratch(&sc));
-  const int64_t limit = max_iters >= 0 ? max_iters : std::min<int64_t>(10 * 2 * n, kPcgIterCap);
-  const int sum2[2] = {RED_SUM, RED_SUM};
   History record{history, max_history};
-  int nb = 0;
-  FL_TRY(pcg2_init(n, sigma1, sigma2, rhs, x, r, pv, sc->partials, &nb, s));
-  // rows: rho -> slot 0, diag form -> slot 3 (finish writes rows contiguously)
-  FL_TRY(finish_reduce(sc->partials, nb, 2, sum2, sc->result, s));
-  FL_CUDA(cudaMemcpyAsync(slots, sc->result, sizeof(double), cudaMemcpyDeviceToDevice, s));
-  FL_CUDA(cudaMemcpyAsync(slots + 3, sc->result + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
-  FL_CUDA(cudaMemcpyAsync(sc->host, slots, sizeof(double), cudaMemcpyDeviceToHost, s));
-  FL_CUDA(cudaStreamSynchronize(s));
-  double rho = sc->host[0];
   FL_TRY(check_rho(rho, 0));
   const double norm0 = std::sqrt(rho);
   const double thr = abs_tol + rel_tol * norm0;
@@ -121,6 +128,23 @@ int pcg_v2(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double
   return FL_OK;
 }
 
+// v2 (host loop): curvature p.Kp = ||Z A p_beta||^2 (reduced inside the fused
+// gram pass) + the diagonal form accumulated where p is written; the update
+// pass reads g = G p_beta and forms K p in registers, so K p never touches
+// HBM.  Per iteration: 2d-1 transform passes + update (104 B/voxel) +
+// p-update (64 B/voxel) = 248 B/voxel in 3D, vs 280 for v1.
+int pcg_v2(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, const double* rhs,
+           double* x, double* work, double abs_tol, double rel_tol, int64_t limit, fl_pcg_result* res,
+           double* history, int64_t max_history, cudaStream_t s) {
+  const int64_t n = p->n;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  int nb = 0;
+  double rho = 0.0;
+  FL_TRY(pcg2_init(n, sigma1, sigma2, rhs, x, work, work + 2 * n, sc->partials, &nb, s));
+  FL_TRY(pcg_start_fetch(sc, nb, false, work + 6 * n, &rho, nullptr, s));
+  return pcg_v2_loop(p, bits, sigma1, sigma2, x, work, rho, abs_tol, rel_tol, limit, res, history, max_history, s);
+}
 
 // ---------------------------------------------------------------------------
 // v3 (default when no host history is requested): the v2 iteration captured
@@ -264,26 +288,14 @@ int pcg_graph(fl_plan_t p, const uint32_t* bits, const double* sigma1, const dou
   return FL_OK;
 }
 
-int pcg_v3(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, const double* rhs,
-           double* x, double* work, double abs_tol, double rel_tol, int64_t max_iters, fl_pcg_result* res,
-           cudaStream_t s) {
+int pcg_v3_loop(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, double* x,
+                double* work, double rho, double abs_tol, double rel_tol, int64_t limit, fl_pcg_result* res,
+                cudaStream_t s) {
   const int64_t n = p->n;
-  double* r = work;
-  double* pv = work + 2 * n;
   double* slots = work + 6 * n;
   PcgCtl* ctl = reinterpret_cast<PcgCtl*>(slots + 8);
   Scratch* sc;
   FL_TRY(scratch(&sc));
-  const int64_t limit = max_iters >= 0 ? max_iters : std::min<int64_t>(10 * 2 * n, kPcgIterCap);
-  const int sum2[2] = {RED_SUM, RED_SUM};
-  int nb = 0;
-  FL_TRY(pcg2_init(n, sigma1, sigma2, rhs, x, r, pv, sc->partials, &nb, s));
-  FL_TRY(finish_reduce(sc->partials, nb, 2, sum2, sc->result, s));
-  FL_CUDA(cudaMemcpyAsync(slots, sc->result, sizeof(double), cudaMemcpyDeviceToDevice, s));
-  FL_CUDA(cudaMemcpyAsync(slots + 3, sc->result + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
-  FL_CUDA(cudaMemcpyAsync(sc->host, slots, sizeof(double), cudaMemcpyDeviceToHost, s));
-  FL_CUDA(cudaStreamSynchronize(s));
-  const double rho = sc->host[0];
   FL_TRY(check_rho(rho, 0));
   const double norm0 = std::sqrt(rho);
   const double thr = abs_tol + rel_tol * norm0;
@@ -310,6 +322,19 @@ int pcg_v3(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double
   res->converged = c.status == 1;
   res->residual_norm = c.norm;
   return FL_OK;
+}
+
+int pcg_v3(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, const double* rhs,
+           double* x, double* work, double abs_tol, double rel_tol, int64_t limit, fl_pcg_result* res,
+           cudaStream_t s) {
+  const int64_t n = p->n;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  int nb = 0;
+  double rho = 0.0;
+  FL_TRY(pcg2_init(n, sigma1, sigma2, rhs, x, work, work + 2 * n, sc->partials, &nb, s));
+  FL_TRY(pcg_start_fetch(sc, nb, false, work + 6 * n, &rho, nullptr, s));
+  return pcg_v3_loop(p, bits, sigma1, sigma2, x, work, rho, abs_tol, rel_tol, limit, res, s);
 }
 
 
@@ -384,6 +409,20 @@ int pcg_v1(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double
   return FL_OK;
 }
 
+int pcg_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("FL_PCG");  // 1: v1, 2: v2 (host loop), default 3 (graph loop)
+    const char* v1 = std::getenv("FL_PCG_V1");
+    if (v1 && v1[0] == '1') return 1;
+    return e ? std::atoi(e) : 3;
+  }();
+  return mode;
+}
+
+int64_t pcg_limit(int64_t n, int64_t max_iters) {
+  return max_iters >= 0 ? max_iters : std::min<int64_t>(10 * 2 * n, kPcgIterCap);
+}
+
 }  // namespace
 
 namespace fl {
@@ -412,17 +451,36 @@ int fl_pcg_kkt(fl_plan_t p, const uint32_t* bits, const double* sigma1, const do
     return fail(FL_E_VALUE, "null argument");
   if (abs_tol < 0 || rel_tol < 0) return fail(FL_E_VALUE, "tolerances must be nonnegative");
   if (abs_tol == 0 && rel_tol == 0) return fail(FL_E_VALUE, "abs_tol and rel_tol cannot both be zero");
-  static const int mode = [] {
-    const char* e = std::getenv("FL_PCG");  // 1: v1, 2: v2 (host loop), default 3 (graph loop)
-    const char* v1 = std::getenv("FL_PCG_V1");
-    if (v1 && v1[0] == '1') return 1;
-    return e ? std::atoi(e) : 3;
-  }();
-  if (mode == 3 && !(history && max_history > 0) && p->n % 2 == 0)
-    return pcg_v3(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, max_iters, res, (cudaStream_t)stream);
-  auto* run = mode == 1 ? pcg_v1 : pcg_v2;
-  return run(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, max_iters, res, history, max_history,
-             (cudaStream_t)stream);
+  const int64_t limit = pcg_limit(p->n, max_iters);
+  const int mode = pcg_mode();
+  cudaStream_t s = (cudaStream_t)stream;
+  if (mode == 1) return pcg_v1(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, limit, res, history,
+                               max_history, s);
+  if (mode == 3 && !(history && max_history > 0))
+    return pcg_v3(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, limit, res, s);
+  return pcg_v2(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, limit, res, history, max_history, s);
+}
+
+int fl_ipm_newton_pcg(fl_plan_t p, const uint32_t* bits, const fl_state* st, const double* g, double lam,
+                      double mu, double* sigma1, double* sigma2, double* x, double* work, double abs_tol,
+                      double rel_tol, int64_t max_iters, fl_pcg_result* res, fl_stream_t stream) {
+  if (!p || !bits || !st || !g || !sigma1 || !sigma2 || !x || !work || !res)
+    return fail(FL_E_VALUE, "null argument");
+  if (abs_tol < 0 || rel_tol < 0) return fail(FL_E_VALUE, "tolerances must be nonnegative");
+  if (abs_tol == 0 && rel_tol == 0) return fail(FL_E_VALUE, "abs_tol and rel_tol cannot both be zero");
+  const int64_t n = p->n;
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  int nb = 0;
+  double rho = 0.0, flag = 0.0;
+  FL_TRY(newton_setup(n, st, g, lam, mu, sigma1, sigma2, x, work, work + 2 * n, sc->partials, &nb, s));
+  FL_TRY(pcg_start_fetch(sc, nb, true, work + 6 * n, &rho, &flag, s));
+  if (flag != 0.0) return fail(FL_E_INTERIOR, "slacks and multipliers must be strictly positive and finite");
+  const int64_t limit = pcg_limit(n, max_iters);
+  if (pcg_mode() == 3)
+    return pcg_v3_loop(p, bits, sigma1, sigma2, x, work, rho, abs_tol, rel_tol, limit, res, s);
+  return pcg_v2_loop(p, bits, sigma1, sigma2, x, work, rho, abs_tol, rel_tol, limit, res, nullptr, 0, s);
 }
 
 }  // extern "C"

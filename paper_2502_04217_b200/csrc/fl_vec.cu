@@ -550,6 +550,49 @@ __global__ void k_pcg2_init(int64_t n, const double* __restrict__ g1, const doub
   emit(dq, SumOp(), red, partials, 1);
 }
 
+// One pass per IPM iteration for everything before the first PCG matvec
+// (ipm.py:303-327): barrier diagonals with the interior check
+// (newton_system.py:72-91), the condensed RHS (:113-145) and the PCG start
+// x = 0, r = rhs, p = P^{-1} r with the rho / diagonal-curvature partials --
+// the same formulas and accumulation order as k_diagonals, k_newton_rhs and
+// k_pcg2_init, so the results are bitwise those of the three-kernel path.
+// Reads 9 n-vectors, writes 8 (136 B/voxel instead of 216).
+__global__ void k_newton_setup(int64_t n, fl_state st, const double* __restrict__ g, double lam, double mu,
+                               double* __restrict__ sig1, double* __restrict__ sig2, double* __restrict__ x,
+                               double* __restrict__ r, double* __restrict__ p, double* __restrict__ partials) {
+  __shared__ double red[32];
+  double rho = 0.0, dq = 0.0, flag = 0.0;
+  GRID_LOOP(i, n) {
+    const double beta = st.beta[i], z = st.z[i], s1 = st.s1[i], s2 = st.s2[i];
+    const double y1 = st.y1[i], y2 = st.y2[i], nu1 = st.nu1[i], nu2 = st.nu2[i];
+    if (bad(s1) || bad(s2) || bad(nu1) || bad(nu2)) flag = 1.0;
+    const double g1 = dvd(nu1, s1), g2 = dvd(nu2, s2);
+    sig1[i] = g1;
+    sig2[i] = g2;
+    const double r1 = sub(add(g[i], y1), y2);
+    const double r2 = sub(add(y1, y2), lam);
+    const double r3 = sub(y1, dvd(mu, s1));
+    const double r4 = sub(y2, dvd(mu, s2));
+    const double r5 = sub(add(z, beta), s1);
+    const double r6 = sub(sub(z, beta), s2);
+    const double rb = add(sub(add(sub(r1, r3), r4), mul(g1, r5)), mul(g2, r6));
+    const double rc = sub(sub(sub(sub(r2, r3), r4), mul(g1, r5)), mul(g2, r6));
+    const Pinv P(g1, g2);
+    const double zt = P.top(rb, rc), zb = P.bot(rb, rc);
+    x[i] = 0.0;
+    x[n + i] = 0.0;
+    r[i] = rb;
+    r[n + i] = rc;
+    p[i] = zt;
+    p[n + i] = zb;
+    rho += mul(rb, zt) + mul(rc, zb);
+    dq += diag_quad(P.l1, P.l2, zt, zb);
+  }
+  emit(rho, SumOp(), red, partials, 0);
+  emit(dq, SumOp(), red, partials, 1);
+  emit(flag, MaxOp(), red, partials, 2);
+}
+
 // x += alpha p; r -= alpha K p with K p formed in registers from g = G p_beta
 // exactly as apply_kkt (newton_system.py:150-151); z = P^{-1} r; rho partials.
 // 16-byte accesses: each thread handles voxels (2i, 2i+1) of both blocks.
@@ -723,6 +766,15 @@ int pcg2_init(int64_t n, const double* sig1, const double* sig2, const double* r
               double* p, double* partials, int* nblocks, cudaStream_t s) {
   const int grid = grid_for(n, T);
   k_pcg2_init<<<grid, T, 0, s>>>(n, sig1, sig2, rhs, x, r, p, partials);
+  FL_LAUNCH_CHECK();
+  *nblocks = grid;
+  return FL_OK;
+}
+
+int newton_setup(int64_t n, const fl_state* st, const double* g, double lam, double mu, double* sig1,
+                 double* sig2, double* x, double* r, double* p, double* partials, int* nblocks, cudaStream_t s) {
+  const int grid = grid_for(n, T);
+  k_newton_setup<<<grid, T, 0, s>>>(n, *st, g, lam, mu, sig1, sig2, x, r, p, partials);
   FL_LAUNCH_CHECK();
   *nblocks = grid;
   return FL_OK;

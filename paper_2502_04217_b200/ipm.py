@@ -35,7 +35,7 @@ from .newton_system import (
     fl_state,
     newton_rhs,
 )
-from .pcg import PcgConfig, kkt_pcg
+from .pcg import PcgConfig, PcgResult, kkt_pcg
 
 __all__ = [
     "IpmConfig",
@@ -428,14 +428,13 @@ def next_barrier(mu: float, tol: float, config: IpmConfig) -> float:
 # ---------------------------------------------------------------------------
 
 class Workspace:
-    """Every device vector one solve needs (about 21 n doubles)."""
+    """Every device vector one solve needs (about 19 n doubles)."""
 
     def __init__(self, n: int):
         self.state = IpmState(mu=0.0, **{f: _dev.empty(n) for f in FIELDS})
         self.sig1 = _dev.empty(n)
         self.sig2 = _dev.empty(n)
         self.g = _dev.empty(n)
-        self.rhs = _dev.empty(2 * n)
         self.x = _dev.empty(2 * n)
         self.work = _dev.empty(_lib.lib().fl_pcg_work_doubles(n))
         self.best_beta = _dev.empty(n)
@@ -443,16 +442,21 @@ class Workspace:
 
 
 def _fused_step(prob: Problem, ws: Workspace, mu: float, lam: float, config: IpmConfig):
-    """ipm_step (ipm.py:364-394) with every vector op fused on the device."""
+    """ipm_step (ipm.py:364-394) with every vector op fused on the device.
+
+    ``fl_ipm_newton_pcg`` is the front half of newton_direction: one pass for
+    the barrier diagonals (interior check), the condensed RHS and the PCG
+    start, then the device-looped PCG (ipm.py:303-332).
+    """
     n = prob.n
-    st = ws.state
     s = _dev.stream()
-    _lib.call("fl_barrier_diagonals", n, _dev.ptr(st.s1), _dev.ptr(st.s2), _dev.ptr(st.nu1),
-              _dev.ptr(st.nu2), _dev.ptr(ws.sig1), _dev.ptr(ws.sig2), None, None, None, None, s)
-    _lib.call("fl_newton_rhs", n, ctypes.byref(ws.fs), _dev.ptr(ws.g), _dev.ptr(ws.sig1),
-              _dev.ptr(ws.sig2), float(lam), float(mu), None, None, None, None, None, None,
-              _dev.ptr(ws.rhs[:n]), _dev.ptr(ws.rhs[n:]), s)
-    res = kkt_pcg(prob.plan, prob.dmask, ws.sig1, ws.sig2, ws.rhs, ws.x, ws.work, _pcg_config(config))
+    pc = _pcg_config(config)
+    out = _lib.FlPcgResult()
+    _lib.call("fl_ipm_newton_pcg", prob.plan.handle, _dev.ptr(prob.dmask.bits), ctypes.byref(ws.fs),
+              _dev.ptr(ws.g), float(lam), float(mu), _dev.ptr(ws.sig1), _dev.ptr(ws.sig2), _dev.ptr(ws.x),
+              _dev.ptr(ws.work), float(pc.abs_tol), float(pc.rel_tol), int(pc.iteration_limit(2 * n)),
+              ctypes.byref(out), s)
+    res = PcgResult(ws.x, int(out.iterations), bool(out.converged), float(out.residual_norm), None)
     if not res.converged:
         raise NumericalBreakdownError(
             f"PCG stalled at preconditioned residual {res.residual_norm:.3e} "

@@ -317,3 +317,48 @@ def test_pcg_graph_loop_breakdown_and_cap():
     s2 = torch.from_numpy(np.abs(rng.standard_normal(n)) + 0.1).cuda()
     res = kkt_pcg(plan, dm, s1, s2, rhs, x, work, PcgConfig(abs_tol=1e-30, max_iters=2))
     assert res.iterations == 2 and not res.converged
+
+
+def test_fused_newton_front_half_bitwise():
+    """fl_ipm_newton_pcg (one setup pass + PCG) == barrier_diagonals + newton_rhs
+    + kkt_pcg, bitwise, on the reference's Newton fixtures; and it raises
+    InteriorViolationError on a non-interior state like barrier_diagonals."""
+    import ctypes
+
+    from paper_2502_04217_b200 import _dev, _lib
+
+    g = load_golden("newton")
+    for dims, _ in json.loads(str(g["cases_json"])):
+        key = "x".join(map(str, dims))
+        n = int(np.prod(dims))
+        if n % 2:
+            continue
+        mask = fl.Mask(g[key + "__missing"], fl.GridShape(dims))
+        lam, mu = float(g[key + "__lam"]), float(g[key + "__mu"])
+        st = ipm.IpmState(mu=mu, **{f: g[f"{key}__st_{f}"] for f in ipm.FIELDS})
+        ref = ipm.newton_direction(st, g[key + "__b"], mask, lam, ipm.IpmConfig(lam=lam))
+        dst = ipm.as_device_state(st)
+        prob = ipm.Problem(g[key + "__b"], mask)
+        gv = prob.residual_adjoint(dst.beta, _dev.empty(n))
+        s1, s2, x = _dev.empty(n), _dev.empty(n), _dev.empty(2 * n)
+        work = _dev.empty(_lib.lib().fl_pcg_work_doubles(n))
+        out = _lib.FlPcgResult()
+        fs = ns.fl_state(dst)
+        _lib.call("fl_ipm_newton_pcg", prob.plan.handle, _dev.ptr(prob.dmask.bits), ctypes.byref(fs),
+                  _dev.ptr(gv), lam, mu, _dev.ptr(s1), _dev.ptr(s2), _dev.ptr(x), _dev.ptr(work),
+                  1e-12, 0.0, 5000, ctypes.byref(out), _dev.stream())
+        assert out.iterations == ref.krylov_iters
+        xh = x.cpu().numpy()
+        assert xh[:n].tobytes() == np.asarray(ref.d_beta).tobytes()
+        assert xh[n:].tobytes() == np.asarray(ref.d_z).tobytes()
+        d = ns.barrier_diagonals(st.s1, st.s2, st.nu1, st.nu2)
+        assert s1.cpu().numpy().tobytes() == d.sigma1.tobytes()
+        s1_bad = np.array(st.s1, copy=True)
+        s1_bad[0] = -1.0
+        dbad = ipm.as_device_state(ipm.IpmState(mu=mu, **{f: (s1_bad if f == "s1" else getattr(st, f))
+                                                          for f in ipm.FIELDS}))
+        fsb = ns.fl_state(dbad)
+        with pytest.raises(fl.InteriorViolationError):
+            _lib.call("fl_ipm_newton_pcg", prob.plan.handle, _dev.ptr(prob.dmask.bits), ctypes.byref(fsb),
+                      _dev.ptr(gv), lam, mu, _dev.ptr(s1), _dev.ptr(s2), _dev.ptr(x), _dev.ptr(work),
+                      1e-12, 0.0, 5000, ctypes.byref(out), _dev.stream())
