@@ -14,9 +14,13 @@ Block structure (newton_system.py:1-36):
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
+import numpy as np
+
 from . import _dev, _lib
+from .errors import UnsupportedShapeError
 from .masking import Mask, embed_device
 
 __all__ = [
@@ -105,10 +109,92 @@ def newton_rhs(state, b, mask: Mask, lam: float) -> KktRhs:
     return KktRhs(*(_dev.out(t, host) for t in outs))
 
 
+_STREAM_MIN = 1 << 20  # host-data calls at least this large stream through PCIe in chunks
+_STREAM_CHUNKS = 8
+_copy_streams: dict = {}
+
+
+def _host_tensor(x, n):
+    import torch
+
+    if isinstance(x, torch.Tensor):
+        t = x.detach().reshape(-1)
+        return t if t.dtype == torch.float64 and t.is_contiguous() else t.to(torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1)))
+
+
+def _apply_kkt_streamed(d_beta, d_z, diag: BarrierDiagonals, mask: Mask):
+    """apply_kkt for host inputs: PCIe transfers overlapped with the work.
+
+    d_beta goes up first and the gram runs on it while d_z streams up in
+    chunks; each chunk's epilogue (top needs g and d_z, bottom needs d_beta
+    and d_z) runs as soon as the chunk lands and its results stream back on
+    a third stream, so the device->host traffic overlaps the host->device
+    traffic (PCIe is full duplex).  Same kernels as the device path, results
+    bitwise equal.
+    """
+    import torch
+
+    n = mask.shape.n
+    hb, hz = _host_tensor(d_beta, n), _host_tensor(d_z, n)
+    if hb.numel() != n or hz.numel() != n:
+        raise UnsupportedShapeError(f"direction blocks must have {n} entries")
+    dev = _dev.device()
+    h2d, d2h = _copy_streams.setdefault(dev.index, (torch.cuda.Stream(dev), torch.cuda.Stream(dev)))
+    comp = torch.cuda.current_stream()
+    g1, g2 = _vec(diag.sigma1, n), _vec(diag.sigma2, n)
+    db, dz, top, bot = (_dev.empty(n) for _ in range(4))
+    out_t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    out_b = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    step = -(-n // _STREAM_CHUNKS)
+    step += step % 2  # 16-byte epilogue accesses
+    bounds = [(a, min(n, a + step)) for a in range(0, n, step)]
+    h2d.wait_stream(comp)  # the device buffers were allocated on the compute stream
+    with torch.cuda.stream(h2d):
+        db.copy_(hb, non_blocking=True)
+        ev_b = torch.cuda.Event()
+        ev_b.record(h2d)
+        ev_z = []
+        for a, b in bounds:
+            dz[a:b].copy_(hz[a:b], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(h2d)
+            ev_z.append(e)
+    plan = _dev.plan_for(mask.shape.dims)
+    dm = mask.on_device()
+    comp.wait_event(ev_b)
+    _lib.call("fl_gram", plan.handle, _dev.ptr(dm.bits), _dev.ptr(db), _dev.ptr(top), _dev.stream())
+    sz = 8  # bytes per double
+    for (a, b), e in zip(bounds, ev_z):
+        comp.wait_event(e)
+        off = a * sz
+        _lib.call("fl_kkt_epilogue", b - a, ctypes.c_void_p(top.data_ptr() + off),
+                  ctypes.c_void_p(db.data_ptr() + off), ctypes.c_void_p(dz.data_ptr() + off),
+                  ctypes.c_void_p(g1.data_ptr() + off), ctypes.c_void_p(g2.data_ptr() + off),
+                  ctypes.c_void_p(bot.data_ptr() + off), None, _dev.stream())
+        done = torch.cuda.Event()
+        done.record(comp)
+        d2h.wait_event(done)
+        with torch.cuda.stream(d2h):
+            out_t[a:b].copy_(top[a:b], non_blocking=True)
+            out_b[a:b].copy_(bot[a:b], non_blocking=True)
+    d2h.synchronize()
+    for t in (db, dz, top, bot):  # keep the caching allocator stream-safe
+        t.record_stream(h2d)
+        t.record_stream(d2h)
+    return out_t.numpy(), out_b.numpy()
+
+
 def apply_kkt(d_beta, d_z, diag: BarrierDiagonals, mask: Mask):
-    """(top, bottom) = K (d_beta, d_z) (newton_system.py:148-152), one fused operator."""
+    """(top, bottom) = K (d_beta, d_z) (newton_system.py:148-152), one fused operator.
+
+    Host inputs (NumPy or CPU tensors) at n >= 2^20 take the streamed path:
+    PCIe uploads, the operator and the downloads overlap chunk by chunk.
+    """
     host = not _dev.is_device(d_beta)
     n = mask.shape.n
+    if host and not _dev.is_device(d_z) and n % 2 == 0 and n >= _STREAM_MIN:
+        return _apply_kkt_streamed(d_beta, d_z, diag, mask)
     db, dz = _vec(d_beta, n), _vec(d_z, n)
     top, bot = _dev.empty(n), _dev.empty(n)
     plan = _dev.plan_for(mask.shape.dims)

@@ -185,3 +185,28 @@ def test_large_grid_matches_oracle(dims):
     assert np.max(np.abs(fl.gram(beta, mask) - orc.gram(beta, om))) <= tol
     w = rng.standard_normal(mask.n_observed)
     assert np.max(np.abs(fl.observe_adjoint(w, mask) - orc.observe_adjoint(w, om))) <= 1e-12 * np.abs(w).max()
+
+
+def test_apply_kkt_streamed_host_path_bitwise(rng):
+    """Host inputs at n >= 2^20 take the chunked, PCIe-overlapped path: same
+    results, bit for bit, as the device-resident call (NumPy and pinned CPU
+    tensors)."""
+    import torch
+
+    from paper_2502_04217_b200 import workloads
+
+    dims = (128, 128, 128)
+    shape = fl.GridShape(dims)
+    mask = fl.Mask.from_bool(workloads.bragg_flags(128), shape)
+    n = shape.n
+    s = [rng.random(n) + 0.4 for _ in range(4)]
+    d = ns.barrier_diagonals(*s)
+    db, dz = rng.standard_normal(n), rng.standard_normal(n)
+    t_dev, b_dev = ns.apply_kkt(torch.from_numpy(db).cuda(), torch.from_numpy(dz).cuda(), d, mask)
+    ref_t, ref_b = t_dev.cpu().numpy(), b_dev.cpu().numpy()
+    t_np, b_np = ns.apply_kkt(db, dz, d, mask)
+    assert t_np.tobytes() == ref_t.tobytes() and b_np.tobytes() == ref_b.tobytes()
+    pb = torch.from_numpy(db).pin_memory()
+    pz = torch.from_numpy(dz).pin_memory()
+    t_p, b_p = ns.apply_kkt(pb, pz, d, mask)
+    assert t_p.tobytes() == ref_t.tobytes() and b_p.tobytes() == ref_b.tobytes()
