@@ -54,10 +54,52 @@ def to_dev(x, n: int | None = None, what: str = "vector"):
             t = t.contiguous()
     else:
         a = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
-        t = torch.from_numpy(a).to(dev)
+        t = _upload(a, dev) if a.nbytes >= _UPLOAD_MIN else torch.from_numpy(a).to(dev)
     if n is not None and t.numel() != n:
         raise UnsupportedShapeError(f"{what} has {t.numel()} entries, expected {n}")
     return t
+
+
+_UPLOAD_MIN = 32 << 20
+_UPLOAD_CHUNK = 64 << 20
+_pool = None
+_side_streams: dict = {}
+
+
+def _upload(a: np.ndarray, dev):
+    """Host->device copy of a large pageable NumPy array.
+
+    A pageable source forces the driver through its own small bounce buffer
+    (~10 GB/s).  Instead, worker threads copy 64 MiB chunks into pinned
+    buffers (NumPy releases the GIL in the copy) while each finished chunk
+    is already DMA-ing up on a side stream; the current stream then waits
+    for the side stream.
+    """
+    global _pool
+    from concurrent.futures import ThreadPoolExecutor
+
+    if _pool is None:
+        _pool = ThreadPoolExecutor(max_workers=4, thread_name_prefix="fl-upload")
+    out = torch.empty(a.size, dtype=F64, device=dev)
+    stage = torch.empty(a.size, dtype=F64, pin_memory=True)
+    hs = stage.numpy()
+    step = _UPLOAD_CHUNK // 8
+    bounds = [(i, min(a.size, i + step)) for i in range(0, a.size, step)]
+
+    def fill(ab):
+        np.copyto(hs[ab[0]:ab[1]], a[ab[0]:ab[1]])
+        return ab
+
+    side = _side_streams.get(dev.index)
+    if side is None:
+        side = _side_streams[dev.index] = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for lo, hi in _pool.map(fill, bounds):
+            out[lo:hi].copy_(stage[lo:hi], non_blocking=True)
+    torch.cuda.current_stream(dev).wait_stream(side)
+    out.record_stream(side)  # (torch's host allocator tracks the pinned stage itself)
+    return out
 
 
 def empty(n: int):

@@ -210,3 +210,21 @@ def test_apply_kkt_streamed_host_path_bitwise(rng):
     pz = torch.from_numpy(dz).pin_memory()
     t_p, b_p = ns.apply_kkt(pb, pz, d, mask)
     assert t_p.tobytes() == ref_t.tobytes() and b_p.tobytes() == ref_b.tobytes()
+
+
+def test_large_numpy_upload_exact(rng):
+    """Pageable NumPy inputs >= 32 MiB go up through pinned chunks on a side
+    stream (ordered before the consuming kernels): exact round trip and the
+    same operator results as a device input."""
+    import torch
+
+    from paper_2502_04217_b200 import _dev
+
+    x = rng.standard_normal((1 << 22) + 6)  # 32 MiB + 48 B: ragged last chunk
+    t = _dev.to_dev(x)
+    assert t.cpu().numpy().tobytes() == x.tobytes()
+    shape = fl.GridShape((256, 128, 128))
+    beta = rng.standard_normal(shape.n)
+    a = fl.synthesize(beta, shape)
+    b = fl.synthesize(torch.from_numpy(beta).cuda(), shape).cpu().numpy()
+    assert a.tobytes() == b.tobytes()
