@@ -42,8 +42,12 @@ def is_device(x) -> bool:
     return isinstance(x, torch.Tensor) and x.is_cuda
 
 
-def to_dev(x, n: int | None = None, what: str = "vector"):
-    """Flat contiguous float64 CUDA tensor view/copy of ``x``."""
+def to_dev(x, n: int | None = None, what: str = "vector", scratch=None):
+    """Flat contiguous float64 CUDA tensor view/copy of ``x``.
+
+    ``scratch`` (a CUDA float64 tensor) may receive the upload of host data
+    instead of a fresh allocation (the solver lends its PCG work buffer).
+    """
     dev = device()
     if isinstance(x, torch.Tensor):
         t = x.detach()
@@ -54,7 +58,13 @@ def to_dev(x, n: int | None = None, what: str = "vector"):
             t = t.contiguous()
     else:
         a = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
-        t = _upload(a, dev) if a.nbytes >= _UPLOAD_MIN else torch.from_numpy(a).to(dev)
+        out = scratch[:a.size] if scratch is not None and scratch.numel() >= a.size else None
+        if a.nbytes >= _UPLOAD_MIN:
+            t = _upload(a, dev, out)
+        elif out is not None:
+            t = out.copy_(torch.from_numpy(a))
+        else:
+            t = torch.from_numpy(a).to(dev)
     if n is not None and t.numel() != n:
         raise UnsupportedShapeError(f"{what} has {t.numel()} entries, expected {n}")
     return t
@@ -66,7 +76,7 @@ _pool = None
 _side_streams: dict = {}
 
 
-def _upload(a: np.ndarray, dev):
+def _upload(a: np.ndarray, dev, out=None):
     """Host->device copy of a large pageable NumPy array.
 
     A pageable source forces the driver through its own small bounce buffer
@@ -80,7 +90,8 @@ def _upload(a: np.ndarray, dev):
 
     if _pool is None:
         _pool = ThreadPoolExecutor(max_workers=4, thread_name_prefix="fl-upload")
-    out = torch.empty(a.size, dtype=F64, device=dev)
+    if out is None:
+        out = torch.empty(a.size, dtype=F64, device=dev)
     stage = torch.empty(a.size, dtype=F64, pin_memory=True)
     hs = stage.numpy()
     step = _UPLOAD_CHUNK // 8
@@ -110,18 +121,66 @@ def zeros(n: int):
     return torch.zeros(int(n), dtype=F64, device=device())
 
 
+_DOWNLOAD_RING_MIN = 1 << 30
+
+
 def out(t, like_host: bool):
     """Return ``t`` as NumPy when the caller passed host data.
 
     The device->host copy lands in page-locked memory from torch's caching
     host allocator (full-bandwidth DMA; freed results are recycled by later
-    calls), exposed to the caller as a NumPy view.
+    calls), exposed to the caller as a NumPy view.  Results of 1 GiB and
+    more go through a ring of pinned 64 MiB chunks into an ordinary NumPy
+    array instead (pinning many GB per call costs seconds).
     """
     if not like_host:
         return t
+    if t.numel() * t.element_size() >= _DOWNLOAD_RING_MIN and t.dtype == F64 and t.is_contiguous():
+        return _download(t).reshape(tuple(t.shape))
     h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     h.copy_(t)
     return h.numpy()
+
+
+def _download(t):
+    """Device->host through 4 pinned 64 MiB slots; worker threads move each
+    landed chunk into the result while later chunks are still in flight."""
+    global _pool
+    from concurrent.futures import ThreadPoolExecutor
+
+    if _pool is None:
+        _pool = ThreadPoolExecutor(max_workers=4, thread_name_prefix="fl-upload")
+    flat = t.reshape(-1)
+    res = np.empty(flat.numel(), dtype=np.float64)
+    step = _UPLOAD_CHUNK // 8
+    nslot = 4
+    ring = [torch.empty(step, dtype=F64, pin_memory=True) for _ in range(nslot)]
+    dev = flat.device
+    side = _side_streams.get(dev.index)
+    if side is None:
+        side = _side_streams[dev.index] = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    pending = [None] * nslot
+
+    def drain(ev, k, lo, hi):
+        ev.synchronize()
+        np.copyto(res[lo:hi], ring[k].numpy()[:hi - lo])
+
+    for i, lo in enumerate(range(0, flat.numel(), step)):
+        hi = min(flat.numel(), lo + step)
+        k = i % nslot
+        if pending[k] is not None:
+            pending[k].result()
+        with torch.cuda.stream(side):
+            ring[k][:hi - lo].copy_(flat[lo:hi], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        pending[k] = _pool.submit(drain, ev, k, lo, hi)
+    for f in pending:
+        if f is not None:
+            f.result()
+    flat.record_stream(side)
+    return res
 
 
 class Plan:

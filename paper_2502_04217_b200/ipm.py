@@ -237,13 +237,14 @@ class SolveReport:
 class Problem:
     """Device-resident (plan, mask bits, embedded observations) of one instance."""
 
-    def __init__(self, b, mask: Mask):
+    def __init__(self, b, mask: Mask, scratch=None):
         self.mask = mask
         self.n = mask.shape.n
         self.plan = _dev.plan_for(mask.shape.dims)
         self.dmask = mask.on_device()
-        self.b = _dev.to_dev(b, mask.n_observed, "observed vector")
-        self.bhat = embed_device(self.b, mask)
+        # only the embedded b_hat stays resident: host observations are uploaded
+        # into ``scratch`` (the solver's PCG work buffer) and embedded from there
+        self.bhat = embed_device(_dev.to_dev(b, mask.n_observed, "observed vector", scratch=scratch), mask)
 
     def residual_adjoint(self, beta, out):
         """out = A^T Z (b_hat - A beta); beta None -> A^T b_hat."""
@@ -252,8 +253,8 @@ class Problem:
                   _dev.ptr(out), _dev.stream())
         return out
 
-    def default_penalty(self) -> float:
-        g = self.residual_adjoint(None, _dev.empty(self.n))
+    def default_penalty(self, scratch=None) -> float:
+        g = self.residual_adjoint(None, scratch if scratch is not None else _dev.empty(self.n))
         m = ctypes.c_double()
         _lib.call("fl_max_abs", self.n, _dev.ptr(g), ctypes.byref(m), _dev.stream())
         return 0.1 * float(m.value)
@@ -355,7 +356,7 @@ def newton_direction(state: IpmState, b, mask: Mask, lam: float,
     prob = Problem(b, mask)
     n = prob.n
     diag = barrier_diagonals(st.s1, st.s2, st.nu1, st.nu2)
-    rhs = newton_rhs(st, prob.b, mask, lam)
+    rhs = newton_rhs(st, b, mask, lam)
     rhs2n = _dev.empty(2 * n)
     rhs2n[:n].copy_(rhs.r_beta)
     rhs2n[n:].copy_(rhs.r_c)
@@ -428,15 +429,22 @@ def next_barrier(mu: float, tol: float, config: IpmConfig) -> float:
 # ---------------------------------------------------------------------------
 
 class Workspace:
-    """Every device vector one solve needs (about 19 n doubles)."""
+    """Every device vector one solve needs: 19 n doubles (+ b_hat in Problem).
+
+    g = A^T Z (b_hat - A beta) lives in the PCG work buffer's G p slot
+    (work[4n:5n]): it is consumed by the Newton setup pass before the PCG
+    loop overwrites that slot and recomputed after the state update, so the
+    two never overlap in time.  20 n doubles = 160 B/voxel in total: 21.5 GB
+    at 512^3, 172 GB at 1024^3 (C5 fits one 180 GB B200).
+    """
 
     def __init__(self, n: int):
         self.state = IpmState(mu=0.0, **{f: _dev.empty(n) for f in FIELDS})
         self.sig1 = _dev.empty(n)
         self.sig2 = _dev.empty(n)
-        self.g = _dev.empty(n)
         self.x = _dev.empty(2 * n)
         self.work = _dev.empty(_lib.lib().fl_pcg_work_doubles(n))
+        self.g = self.work[4 * n:5 * n]
         self.best_beta = _dev.empty(n)
         self.fs = fl_state(self.state)
 
@@ -484,12 +492,16 @@ def solve(b, mask: Mask, config: IpmConfig = IpmConfig(),
     observer); a CUDA tensor ``b`` keeps everything on the device.
     """
     host = not _dev.is_device(b)
-    prob = Problem(b, mask)
-    n = prob.n
-    lam = config.lam if config.lam is not None else prob.default_penalty()
+    if config.lam is not None and config.lam <= 0:
+        raise ValueError("penalty must be positive")
+    n = mask.shape.n
+    # the 19 n-double workspace first; its PCG buffer then stages the upload
+    # of host observations, so the peak is the workspace + b_hat (20 n)
+    ws = Workspace(n)
+    prob = Problem(b, mask, scratch=ws.work)
+    lam = config.lam if config.lam is not None else prob.default_penalty(ws.g)
     if lam <= 0:
         raise ValueError("penalty must be positive")
-    ws = Workspace(n)
     st = ws.state
     st.mu = lam / 2.0 if config.mu_init is None else float(config.mu_init)
     _lib.call("fl_ipm_init", n, ctypes.byref(ws.fs), float(lam), _dev.stream())

@@ -228,3 +228,17 @@ def test_large_numpy_upload_exact(rng):
     a = fl.synthesize(beta, shape)
     b = fl.synthesize(torch.from_numpy(beta).cuda(), shape).cpu().numpy()
     assert a.tobytes() == b.tobytes()
+
+
+def test_large_download_ring_exact(rng):
+    """Results >= 1 GiB come back through the pinned ring into a NumPy array."""
+    import torch
+
+    from paper_2502_04217_b200 import _dev
+
+    n = (1 << 27) + 10  # 1 GiB + 80 B: ragged last chunk
+    g = torch.Generator(device="cuda").manual_seed(7)
+    t = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    h = _dev.out(t, True)
+    assert isinstance(h, np.ndarray) and h.shape == (n,)
+    assert h.tobytes() == t.cpu().numpy().tobytes()

@@ -1,6 +1,6 @@
-"""One warm C4 solve at side^3 (for an ncu launch list of the IPM/PCG kernels).
+"""IPM solves of a BASELINE recipe (for an ncu launch list of the IPM/PCG kernels).
 
-    python tools/profile_solve.py [--size 512]
+    python tools/profile_solve.py [--config c4] [--size 512] [--reps 1]
 """
 import argparse
 import os
@@ -16,12 +16,16 @@ from paper_2502_04217_b200 import workloads  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--size", type=int, default=512)
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--reps", type=int, default=1)
     a = ap.parse_args()
-    inst = workloads.c4_const(a.size)
+    inst = {"c1": lambda: workloads.c1_1d(seed=0), "c2": lambda: workloads.c2_2d(seed=0),
+            "c3": lambda: workloads.c3_bragg(a.size, seed=0), "c4": lambda: workloads.c4_const(a.size)}[a.config]()
     mask = fl.Mask.from_bool(inst.flags, fl.GridShape(inst.dims))
     b = fl.observe(torch.from_numpy(inst.beta_true).cuda(), mask)
     b += torch.from_numpy(inst.noise).cuda()
-    beta, rep = fl.solve(b, mask, fl.IpmConfig(lam=inst.lam))
+    for _ in range(a.reps):
+        beta, rep = fl.solve(b, mask, fl.IpmConfig(lam=inst.lam))
     torch.cuda.synchronize()
     print(f"ok: {rep.status} {rep.iterations} IPM, krylov {rep.krylov_counts}", flush=True)
 
