@@ -278,6 +278,8 @@ def run_b200(args, rank: int, world: int):
     if not args.no_solve:
         solve_info = run_solve(args.solve_size, barrier)
         other = run_other_solves(barrier)
+        if not args.no_c5:
+            other["C5 1024^3 Bragg, lambda=0.5, ONE GPU"] = run_c5(barrier)
     return dict(value=value, ms_per_step=ms_per_step, roofline=roofline, roofline_operator=roofline_op,
                 passes=passes, clocks=clock, e2e=e2e, solve=solve_info, other=other,
                 gpu_launches=args.steps * npass)
@@ -406,14 +408,19 @@ def _solve_instance(inst, barrier, reps_warm=1, ista=False):
     del b, bt, beta
     torch.cuda.empty_cache()
     barrier()
-    t0 = time.perf_counter()
-    beta_h, rep2 = fl.solve(b_host, mask, cfg)
-    e2e_s = time.perf_counter() - t0
+    e2e_runs = []
+    for _ in range(2):  # steady state: the first call also pins the host staging
+        beta_h = None
+        t0 = time.perf_counter()
+        beta_h, rep2 = fl.solve(b_host, mask, cfg)
+        e2e_runs.append(time.perf_counter() - t0)
+    e2e_s = min(e2e_runs)
     true_support = np.flatnonzero(inst.beta_true)
     found = np.flatnonzero(np.abs(beta_h) > 1e-6 * np.max(np.abs(beta_h)))
     return {"status": rep.status, "lambda": rep.lam, "ipm_iterations": rep.iterations,
             "krylov": rep.krylov_counts, "total_krylov": rep.total_krylov,
             "device_s_cold": round(cold, 4), "device_s": round(min(warm), 4), "e2e_s": round(e2e_s, 4),
+            "e2e_s_first": round(e2e_runs[0], 4),
             "final_objective": rep.final_objective,
             "support_exact": bool(np.array_equal(found, true_support)), "n_support": int(found.size),
             **({"ista_crosscheck": cross} if ista else {})}
@@ -441,6 +448,47 @@ def run_other_solves(barrier):
         except Exception as exc:  # report, never hide, a failing config
             res[name] = {"error": repr(exc)[:300]}
     return res
+
+
+def run_c5(barrier):
+    """C5 (1024^3, constant amplitudes, lambda 0.5) on ONE GPU: the solver's
+    device footprint is 20 n doubles = 172 GB (SURVEY sizes C5 for 8 GPUs)."""
+    import torch
+
+    import paper_2502_04217_b200 as fl
+    from paper_2502_04217_b200 import workloads
+
+    torch.cuda.empty_cache()
+    try:
+        inst = workloads.c4_const(1024)
+        mask = fl.Mask.from_bool(inst.flags, fl.GridShape(inst.dims))
+        bt = torch.from_numpy(inst.beta_true).cuda()
+        b = fl.observe(bt, mask)
+        del bt
+        b += torch.from_numpy(inst.noise).cuda()
+        b_host = b.cpu().numpy()
+        del b
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
+        cfg = fl.IpmConfig(lam=inst.lam, tol=1e-8)
+        barrier()
+        t0 = time.perf_counter()
+        beta, rep = fl.solve(b_host, mask, cfg)
+        e2e_s = time.perf_counter() - t0
+        found = np.flatnonzero(np.abs(beta) > 1e-6 * np.max(np.abs(beta)))
+        out = {"status": rep.status, "lambda": rep.lam, "ipm_iterations": rep.iterations,
+               "krylov": rep.krylov_counts, "total_krylov": rep.total_krylov,
+               "device_s": round(rep.wall_time, 4), "e2e_s_first": round(e2e_s, 4),
+               "final_objective": rep.final_objective,
+               "support_exact": bool(np.array_equal(found, np.flatnonzero(inst.beta_true))),
+               "n_support": int(found.size),
+               "device_peak_GB": round(torch.cuda.max_memory_allocated() / 1e9, 1),
+               "note": "device_s = IPM loop (host-synchronised, perf_counter); e2e = NumPy in/out, first call"}
+        del beta, b_host, inst, mask
+    except Exception as exc:  # report, never hide
+        out = {"error": repr(exc)[:300]}
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -511,6 +559,7 @@ def main():
     ap.add_argument("--solve-size", type=int, default=512)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the 1024^3 single-GPU solve")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--ref-budget", type=float, default=150.0)
     ap.add_argument("--emulate", type=int, default=0,
