@@ -290,6 +290,24 @@ FL_API int fl_axpy(int64_t n, double alpha, const double* x, double* y, fl_strea
 /* y = x + beta * y    (NumPy ``p = z + beta * p``) */
 FL_API int fl_xpby(int64_t n, const double* x, double beta, double* y, fl_stream_t stream);
 
+/* ---- slab exchange over peer memory (sharded transform) ------
+ * One kernel per direction instead of pack -> all-to-all -> unpack: each
+ * element of the local slab is stored once, transposed, straight into the
+ * owning rank's slab.  ``y_slabs`` / ``x_slabs`` hold ``nranks`` device
+ * pointers (peer allocations opened with fl_ipc_open; this rank's own buffer
+ * at index ``rank``).  The caller orders the exchange with a cross-rank
+ * barrier on the stream afterwards (e.g. a one-element all-reduce). */
+FL_API int fl_slab_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int nranks, int rank, const double* x_slab,
+                                double* const* y_slabs, fl_stream_t stream);
+FL_API int fl_slab_y_to_x_peers(int64_t a, int64_t b, int64_t d2, int nranks, int rank, const double* y_slab,
+                                double* const* x_slabs, fl_stream_t stream);
+/* cudaMalloc + cudaIpcGetMemHandle (64-byte handle), the peer side's open /
+ * close, and the matching free. */
+FL_API int fl_ipc_alloc(int64_t bytes, void** ptr, unsigned char* handle64);
+FL_API int fl_ipc_open(const unsigned char* handle64, void** ptr);
+FL_API int fl_ipc_close(void* ptr);
+FL_API int fl_dev_free(void* ptr);
+
 /* ---- fused Newton step front half (ipm.py:303-332) ---------------------
  * One pass computes the barrier diagonals sigma = nu/s with the interior
  * check (newton_system.py:72-91 -> FL_E_INTERIOR), the condensed RHS

@@ -7,6 +7,7 @@
 // consume those blocks.  X-side kernels are contiguous runs of d2 (16-byte
 // moves); Y-side kernels transpose (i0, i2) through 32x33 shared tiles.
 #include <algorithm>
+#include <cstring>
 
 #include "fl_common.cuh"
 #include "fl_internal.h"
@@ -79,6 +80,81 @@ __global__ void k_y_blocks(int64_t a, int64_t b, int64_t d2, int P, const double
   }
 }
 
+// ---- fused exchange over peer memory -----------------------------------
+// One kernel per direction replaces pack -> all-to-all -> unpack: every
+// element is read once from the local slab and stored once, transposed, into
+// its final place in the OWNING rank's slab (a peer pointer over NVLink /
+// NVSwitch for remote ranks, the local buffer for this rank).  The 32x33
+// shared tile turns the layout change into 256-byte coalesced row stores on
+// both sides.
+constexpr int kMaxPeers = 16;
+struct Peers {
+  double* p[kMaxPeers];
+};
+
+// X-slab (a, d1, d2) of rank `me` -> Y-slabs (b, d2, d0) of every rank:
+//   Y[j / b][((j % b) d2 + i2) d0 + me a + i0] = x[(i0 d1 + j) d2 + i2]
+// One CTA per (j, 32x32 tile of (i0, i2)).
+__global__ void k_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int P, int me, const double* __restrict__ x,
+                               Peers dst) {
+  __shared__ double tile[32][33];
+  const int64_t b = d1 / P, d0 = a * P;
+  const int64_t t0 = (a + 31) / 32, t2 = (d2 + 31) / 32;
+  int64_t id = blockIdx.x;
+  const int64_t ti2 = id % t2;
+  id /= t2;
+  const int64_t ti0 = id % t0;
+  const int64_t j = id / t0;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t base0 = ti0 * 32, base2 = ti2 * 32;
+  for (int k = ty; k < 32; k += 8) {  // read: i2 fastest
+    const int64_t i0 = base0 + k, i2 = base2 + tx;
+    if (i0 < a && i2 < d2) tile[k][tx] = x[(i0 * d1 + j) * d2 + i2];
+  }
+  __syncthreads();
+  double* y = dst.p[j / b];
+  const int64_t j1 = j % b;
+  for (int k = ty; k < 32; k += 8) {  // write: i0 fastest
+    const int64_t i2 = base2 + k, i0 = base0 + tx;
+    if (i0 < a && i2 < d2) y[(j1 * d2 + i2) * d0 + me * a + i0] = tile[tx][k];
+  }
+}
+
+// Y-slab (b, d2, d0) of rank `me` -> X-slabs (a, d1, d2) of every rank:
+//   X[i / a][((i % a) d1 + me b + j1) d2 + i2] = y[(j1 d2 + i2) d0 + i]
+// One CTA per (j1, 32x32 tile of (i, i2)).
+__global__ void k_y_to_x_peers(int64_t a, int64_t b, int64_t d2, int P, int me, const double* __restrict__ y,
+                               Peers dst) {
+  __shared__ double tile[32][33];
+  const int64_t d0 = a * P, d1 = b * P;
+  const int64_t ti_n = (d0 + 31) / 32, t2 = (d2 + 31) / 32;
+  int64_t id = blockIdx.x;
+  const int64_t ti2 = id % t2;
+  id /= t2;
+  const int64_t ti = id % ti_n;
+  const int64_t j1 = id / ti_n;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t base = ti * 32, base2 = ti2 * 32;
+  for (int k = ty; k < 32; k += 8) {  // read: i fastest
+    const int64_t i2 = base2 + k, i = base + tx;
+    if (i < d0 && i2 < d2) tile[tx][k] = y[(j1 * d2 + i2) * d0 + i];
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {  // write: i2 fastest
+    const int64_t i = base + k, i2 = base2 + tx;
+    if (i < d0 && i2 < d2) dst.p[i / a][((i % a) * d1 + me * b + j1) * d2 + i2] = tile[k][tx];
+  }
+}
+
+int peers_of(int P, double* const* ptrs, Peers* out) {
+  if (P < 1 || P > kMaxPeers) return fail(FL_E_VALUE, "peer exchange supports 1..16 ranks");
+  for (int r = 0; r < P; ++r) {
+    if (!ptrs[r]) return fail(FL_E_VALUE, "null peer pointer");
+    out->p[r] = ptrs[r];
+  }
+  return FL_OK;
+}
+
 int x_blocks(bool pack, int64_t a, int64_t d1, int64_t d2, int P, const double* src, double* dst,
              cudaStream_t s) {
   if (P < 1 || d1 % P || d2 % 2) return fail(FL_E_SHAPE, "slab transpose needs d1 % P == 0 and even d2");
@@ -130,6 +206,64 @@ int fl_slab_pack_y(int64_t a, int64_t b, int64_t d2, int nranks, const double* y
                    fl_stream_t stream) {
   if (!y_slab || !send) return fail(FL_E_VALUE, "null argument");
   return y_blocks(false, a, b, d2, nranks, y_slab, send, (cudaStream_t)stream);
+}
+
+int fl_slab_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int nranks, int rank, const double* x_slab,
+                         double* const* y_slabs, fl_stream_t stream) {
+  if (!x_slab || !y_slabs) return fail(FL_E_VALUE, "null argument");
+  if (nranks < 1 || d1 % nranks || rank < 0 || rank >= nranks) return fail(FL_E_SHAPE, "bad slab geometry");
+  Peers pe;
+  FL_TRY(peers_of(nranks, y_slabs, &pe));
+  const int64_t blocks = d1 * ((a + 31) / 32) * ((d2 + 31) / 32);
+  if (blocks > 0x7fffffffLL) return fail(FL_E_SHAPE, "slab too large");
+  if (blocks == 0) return FL_OK;
+  k_x_to_y_peers<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a, d1, d2, nranks, rank, x_slab, pe);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+int fl_slab_y_to_x_peers(int64_t a, int64_t b, int64_t d2, int nranks, int rank, const double* y_slab,
+                         double* const* x_slabs, fl_stream_t stream) {
+  if (!y_slab || !x_slabs) return fail(FL_E_VALUE, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(FL_E_SHAPE, "bad slab geometry");
+  Peers pe;
+  FL_TRY(peers_of(nranks, x_slabs, &pe));
+  const int64_t blocks = b * ((a * nranks + 31) / 32) * ((d2 + 31) / 32);
+  if (blocks > 0x7fffffffLL) return fail(FL_E_SHAPE, "slab too large");
+  if (blocks == 0) return FL_OK;
+  k_y_to_x_peers<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a, b, d2, nranks, rank, y_slab, pe);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+// Device buffers shareable across processes (cudaMalloc'd, so an IPC handle
+// names exactly this allocation) for the peer exchange.
+int fl_ipc_alloc(int64_t bytes, void** ptr, unsigned char* handle64) {
+  if (!ptr || !handle64 || bytes <= 0) return fail(FL_E_VALUE, "bad argument");
+  FL_CUDA(cudaMalloc(ptr, (size_t)bytes));
+  cudaIpcMemHandle_t h;
+  FL_CUDA(cudaIpcGetMemHandle(&h, *ptr));
+  static_assert(sizeof(h) == 64, "IPC handle is 64 bytes");
+  memcpy(handle64, &h, 64);
+  return FL_OK;
+}
+
+int fl_ipc_open(const unsigned char* handle64, void** ptr) {
+  if (!ptr || !handle64) return fail(FL_E_VALUE, "bad argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  FL_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return FL_OK;
+}
+
+int fl_ipc_close(void* ptr) {
+  if (ptr) FL_CUDA(cudaIpcCloseMemHandle(ptr));
+  return FL_OK;
+}
+
+int fl_dev_free(void* ptr) {
+  if (ptr) FL_CUDA(cudaFree(ptr));
+  return FL_OK;
 }
 
 }  // extern "C"

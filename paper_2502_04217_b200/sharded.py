@@ -25,6 +25,20 @@ P shards of a grid in one process (single-GPU emulation of the sharded
 algorithm -- no kernel ever waits on another rank).  Every operation below
 works on *lists of local shards* (length 1 under DistComm, P under
 LocalComm).
+
+Two exchange implementations (``ShardedGrid(..., exchange=...)``, default
+from ``FL_SHARD_EXCHANGE``):
+
+* ``"a2a"`` (default): pack kernel -> ``all_to_all_single`` (NCCL) -> unpack
+  kernel;
+* ``"peer"``: ONE kernel per direction stores every element, transposed,
+  straight into the owning rank's slab through peer pointers (CUDA IPC
+  buffers opened on every rank; NVLink / NVSwitch stores), followed by a
+  one-element all-reduce as the stream-ordered barrier.  Per element one
+  read and one (remote) write instead of three of each, no send buffer.
+  Validated bit-for-bit against ``"a2a"`` with LocalComm on one GPU (where
+  the "peer" tables are the local shard buffers); the IPC path itself needs
+  two or more GPUs.
 """
 
 from __future__ import annotations
@@ -102,6 +116,15 @@ class Comm:
     def reduce(self, values: list, op: str) -> np.ndarray:
         raise NotImplementedError
 
+    def barrier(self):
+        """Stream-ordered cross-rank barrier (after a peer exchange)."""
+        raise NotImplementedError
+
+    def peer_buffers(self, n: int):
+        """Exchange buffers of ``n`` doubles: (local tensors, pointer tables),
+        one per local shard; table[r] addresses rank r's buffer."""
+        raise NotImplementedError
+
 
 class LocalComm(Comm):
     """All P shards in this process: exchanges are block copies."""
@@ -122,6 +145,14 @@ class LocalComm(Comm):
     def reduce(self, values, op):
         arr = np.array([np.asarray(v, dtype=np.float64).reshape(-1) for v in values])
         return {SUM: arr.sum(0), MAX: arr.max(0), MIN: arr.min(0)}[op]
+
+    def barrier(self):
+        pass  # one stream: the exchange kernels already ran in order
+
+    def peer_buffers(self, n):
+        bufs = [_dev.empty(n) for _ in range(self.world)]
+        table = (ctypes.c_void_p * self.world)(*(b.data_ptr() for b in bufs))
+        return bufs, [table] * self.world
 
 
 class DistComm(Comm):
@@ -151,6 +182,52 @@ class DistComm(Comm):
         rop = {SUM: self.dist.ReduceOp.SUM, MAX: self.dist.ReduceOp.MAX, MIN: self.dist.ReduceOp.MIN}[op]
         self.dist.all_reduce(t, op=rop, group=self.group)
         return t.cpu().numpy()
+
+    def barrier(self):
+        import torch
+
+        # an all-reduce cannot complete on any rank before every rank's stream
+        # reached it, i.e. before every rank's exchange kernel has finished
+        t = torch.zeros(1, dtype=torch.float64, device=self.device if self.device is not None else "cpu")
+        self.dist.all_reduce(t, group=self.group)
+
+    def peer_buffers(self, n):
+        import torch
+
+        ptr = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        _lib.call("fl_ipc_alloc", n * 8, ctypes.byref(ptr), handle)
+        mine = torch.frombuffer(bytearray(handle.raw), dtype=torch.uint8)
+        dev = self.device if self.device is not None else "cpu"
+        gathered = [torch.empty(64, dtype=torch.uint8, device=dev) for _ in range(self.world)]
+        self.dist.all_gather(gathered, mine.to(dev), group=self.group)
+        me = self.ranks[0]
+        ptrs = []
+        for r, h in enumerate(gathered):
+            if r == me:
+                ptrs.append(ptr.value)
+                continue
+            q = ctypes.c_void_p()
+            _lib.call("fl_ipc_open", bytes(h.cpu().numpy().tobytes()), ctypes.byref(q))
+            ptrs.append(q.value)
+            self._opened = getattr(self, "_opened", []) + [q.value]
+        self._owned = getattr(self, "_owned", []) + [ptr.value]
+        table = (ctypes.c_void_p * self.world)(*ptrs)
+        return [_wrap_device(ptr.value, n)], [table]
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device allocation (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                          "version": 3, "strides": None}
+
+
+def _wrap_device(ptr: int, n: int):
+    import torch
+
+    return torch.as_tensor(_CudaArray(ptr, n), device=_dev.device())
 
 
 # ---------------------------------------------------------------------------
@@ -228,6 +305,16 @@ class ShardOps:
         g = self.geo
         _lib.call("fl_slab_unpack_x", g.a, g.dims[1], g.dims[2], g.P, _dev.ptr(recv), _dev.ptr(x), _dev.stream())
 
+    def x_to_y_peers(self, rank, x, table):
+        g = self.geo
+        _lib.call("fl_slab_x_to_y_peers", g.a, g.dims[1], g.dims[2], g.P, rank, _dev.ptr(x),
+                  ctypes.cast(table, ctypes.POINTER(ctypes.c_void_p)), _dev.stream())
+
+    def y_to_x_peers(self, rank, y, table):
+        g = self.geo
+        _lib.call("fl_slab_y_to_x_peers", g.a, g.b, g.dims[2], g.P, rank, _dev.ptr(y),
+                  ctypes.cast(table, ctypes.POINTER(ctypes.c_void_p)), _dev.stream())
+
 
 # ---------------------------------------------------------------------------
 # sharded operators
@@ -236,15 +323,33 @@ class ShardOps:
 class ShardedGrid:
     """Geometry, comm, per-shard ops and exchange buffers of one sharded grid."""
 
-    def __init__(self, dims, comm: Comm, ops_factory=ShardOps):
+    def __init__(self, dims, comm: Comm, ops_factory=ShardOps, exchange=None):
+        import os
+
         self.geo = SlabGeometry(tuple(int(d) for d in dims), comm.world)
         self.comm = comm
         self.ops = [ops_factory(self.geo) for _ in comm.ranks]
         n = self.geo.n_local
-        self.send = [self.ops[0].empty(n) for _ in comm.ranks]
-        self.ybuf = [self.ops[0].empty(n) for _ in comm.ranks]
+        self.exchange = exchange or os.environ.get("FL_SHARD_EXCHANGE", "a2a")
+        if self.exchange not in ("a2a", "peer"):
+            raise ValueError(f"unknown exchange {self.exchange!r}")
+        if self.exchange == "peer":
+            # grid-owned receive slabs, addressable by every rank
+            self.ybuf, self.ytab = comm.peer_buffers(n)
+            self.xrecv, self.xtab = comm.peer_buffers(n)
+        else:
+            self.send = [self.ops[0].empty(n) for _ in comm.ranks]
+            self.ybuf = [self.ops[0].empty(n) for _ in comm.ranks]
 
     def x_to_y(self, xs, ys):
+        if self.exchange == "peer":  # into the grid's Y slabs, then copy if asked elsewhere
+            for i, (op, r, x) in enumerate(zip(self.ops, self.comm.ranks, xs)):
+                op.x_to_y_peers(r, x, self.ytab[i])
+            self.comm.barrier()
+            for y, yb in zip(ys, self.ybuf):
+                if y.data_ptr() != yb.data_ptr():
+                    y.copy_(yb)
+            return
         for op, x, s in zip(self.ops, xs, self.send):
             op.pack_x(x, s)
         recv = self.comm.all_to_all(self.send)
@@ -252,17 +357,26 @@ class ShardedGrid:
             op.unpack_y(rv, y)
 
     def y_to_x(self, ys, xs):
+        """Y slabs -> X slabs; with the peer exchange the result lands in the
+        grid's receive slabs (returned), otherwise in ``xs``."""
+        if self.exchange == "peer":
+            for i, (op, r, y) in enumerate(zip(self.ops, self.comm.ranks, ys)):
+                op.y_to_x_peers(r, y, self.xtab[i])
+            self.comm.barrier()
+            return self.xrecv
         for op, y, s in zip(self.ops, ys, self.send):
             op.pack_y(y, s)
         recv = self.comm.all_to_all(self.send)
         for op, rv, x in zip(self.ops, recv, xs):
             op.unpack_x(rv, x)
+        return xs
 
     def synthesize_to_y(self, betas, ys):
         """A beta with beta in X-slabs; result in Y-slabs (b, d2, d0)."""
-        for op, b, y in zip(self.ops, betas, self.ybuf):
-            op.synth_x(b, y)  # ybuf used as X-layout scratch here
-        self.x_to_y(self.ybuf, ys)
+        scratch = self.xrecv if self.exchange == "peer" else self.ybuf
+        for op, b, x in zip(self.ops, betas, scratch):
+            op.synth_x(b, x)  # X-layout scratch
+        self.x_to_y(scratch, ys)
         for op, y in zip(self.ops, ys):
             op.synth_y0(y, y)
 
@@ -277,9 +391,9 @@ class ShardedGrid:
         norms = []
         for i, (op, y) in enumerate(zip(self.ops, self.ybuf)):
             norms.append(op.fused_y(bits_y[i], None if bhat_y is None else bhat_y[i], y, y, want_norm))
-        self.y_to_x(self.ybuf, outs)
-        for op, o in zip(self.ops, outs):
-            op.analyze_x(o, o)
+        src = self.y_to_x(self.ybuf, outs)
+        for op, x, o in zip(self.ops, src, outs):
+            op.analyze_x(x, o)
         if want_norm:
             return float(self.comm.reduce([[v] for v in norms], SUM)[0])
         return None
