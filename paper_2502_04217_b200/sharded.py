@@ -29,16 +29,16 @@ LocalComm).
 Two exchange implementations (``ShardedGrid(..., exchange=...)``, default
 from ``FL_SHARD_EXCHANGE``):
 
-* ``"a2a"`` (default): pack kernel -> ``all_to_all_single`` (NCCL) -> unpack
-  kernel;
-* ``"peer"``: ONE kernel per direction stores every element, transposed,
+* ``"peer"`` (default; falls back to ``"a2a"`` if peer buffers cannot be
+  set up): ONE kernel per direction stores every element, transposed,
   straight into the owning rank's slab through peer pointers (CUDA IPC
   buffers opened on every rank; NVLink / NVSwitch stores), followed by a
   one-element all-reduce as the stream-ordered barrier.  Per element one
   read and one (remote) write instead of three of each, no send buffer.
   Validated bit-for-bit against ``"a2a"`` with LocalComm on one GPU (where
   the "peer" tables are the local shard buffers); the IPC path itself needs
-  two or more GPUs.
+  two or more GPUs;
+* ``"a2a"``: pack kernel -> ``all_to_all_single`` (NCCL) -> unpack kernel.
 """
 
 from __future__ import annotations
@@ -330,14 +330,22 @@ class ShardedGrid:
         self.comm = comm
         self.ops = [ops_factory(self.geo) for _ in comm.ranks]
         n = self.geo.n_local
-        self.exchange = exchange or os.environ.get("FL_SHARD_EXCHANGE", "a2a")
+        self.exchange = exchange or os.environ.get("FL_SHARD_EXCHANGE", "peer")
         if self.exchange not in ("a2a", "peer"):
             raise ValueError(f"unknown exchange {self.exchange!r}")
         if self.exchange == "peer":
             # grid-owned receive slabs, addressable by every rank
-            self.ybuf, self.ytab = comm.peer_buffers(n)
-            self.xrecv, self.xtab = comm.peer_buffers(n)
-        else:
+            try:
+                self.ybuf, self.ytab = comm.peer_buffers(n)
+                self.xrecv, self.xtab = comm.peer_buffers(n)
+            except (RuntimeError, OSError, ValueError, AttributeError) as exc:
+                if exchange == "peer":  # explicitly requested: do not hide the failure
+                    raise
+                import warnings
+
+                warnings.warn(f"peer exchange unavailable ({exc}); using all-to-all")
+                self.exchange = "a2a"
+        if self.exchange == "a2a":
             self.send = [self.ops[0].empty(n) for _ in comm.ranks]
             self.ybuf = [self.ops[0].empty(n) for _ in comm.ranks]
 

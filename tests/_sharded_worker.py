@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.join(REPO, "tests"))
 import numpy as np  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-from helpers.numpy_shard_ops import NumpyShardOps  # noqa: E402
+from helpers.numpy_shard_ops import NumpyShardOps, ShmPeerComm  # noqa: E402
 from oracle import fftlasso_oracle as orc  # noqa: E402
 from paper_2502_04217_b200.sharded import MAX, MIN, SUM, DistComm, ShardedGrid, ShardedProblem  # noqa: E402
 
@@ -19,9 +19,10 @@ def main():
     dist.init_process_group("gloo")
     r = dist.get_rank()
     out = {}
-    for dims in [(4, 6, 8), (8, 4, 6), (16, 16, 8)]:
-        comm = DistComm()
-        grid = ShardedGrid(dims, comm, ops_factory=NumpyShardOps)
+    raw = {}
+    for dims, exchange in [(d, ex) for d in [(4, 6, 8), (8, 4, 6), (16, 16, 8)] for ex in ("a2a", "peer")]:
+        comm = DistComm() if exchange == "a2a" else ShmPeerComm()
+        grid = ShardedGrid(dims, comm, ops_factory=NumpyShardOps, exchange=exchange)
         geo = grid.geo
         rng = np.random.default_rng(7)  # same on every rank
         n = geo.n
@@ -46,7 +47,11 @@ def main():
         grid.synthesize_to_y(xb, y)
         err_syn = float(np.max(np.abs(y[0].numpy() - geo.y_slab(ax, r))))
         red = [comm.reduce([[float(r + 1)]], op)[0] for op in (SUM, MAX, MIN)]
-        out[str(dims)] = dict(gram=err_gram, norm=err_nrm, resid=err_resid, synth=err_syn, red=red)
+        out[f"{dims} {exchange}"] = dict(gram=err_gram, norm=err_nrm, resid=err_resid, synth=err_syn, red=red)
+        raw[(dims, exchange)] = (g[0].numpy().tobytes(), gr[0].numpy().tobytes(), y[0].numpy().tobytes(), nrm)
+        if exchange == "peer":
+            out[f"{dims} peer==a2a"] = raw[(dims, "peer")] == raw[(dims, "a2a")]
+            comm.close()
     if r == 0:
         print("RESULT " + json.dumps(out), flush=True)
     dist.barrier()

@@ -78,3 +78,56 @@ class NumpyShardOps:
         g = self.geo
         blocks = recv.numpy().reshape(g.P, g.a, g.b, g.dims[2])
         x.copy_(torch.from_numpy(np.ascontiguousarray(blocks.transpose(1, 0, 2, 3)).reshape(-1)))
+
+    # peer exchange: write straight into the owning rank's slab (``table`` holds
+    # every rank's buffer as a NumPy array; see ShmPeerComm)
+    def x_to_y_peers(self, rank, x, table):
+        g = self.geo
+        xs = self._x(x)  # (a, d1, d2)
+        for r2, buf in enumerate(table):
+            y = buf.reshape(g.b, g.dims[2], g.dims[0])
+            y[:, :, rank * g.a:(rank + 1) * g.a] = xs[:, r2 * g.b:(r2 + 1) * g.b, :].transpose(1, 2, 0)
+
+    def y_to_x_peers(self, rank, y, table):
+        g = self.geo
+        ys = self._y(y)  # (b, d2, d0)
+        for r2, buf in enumerate(table):
+            xr = buf.reshape(g.a, g.dims[1], g.dims[2])
+            xr[:, rank * g.b:(rank + 1) * g.b, :] = ys[:, :, r2 * g.a:(r2 + 1) * g.a].transpose(2, 0, 1)
+
+
+class ShmPeerComm:
+    """CPU stand-in for the CUDA-IPC peer buffers of sharded.DistComm: POSIX
+    shared memory created by each rank, names all-gathered over gloo, every
+    rank maps every buffer; the barrier is a gloo barrier.  Everything else
+    is DistComm's."""
+
+    def __new__(cls, *a, **k):
+        from paper_2502_04217_b200.sharded import DistComm
+
+        class _Shm(DistComm):
+            def peer_buffers(self, n):
+                from multiprocessing import shared_memory
+
+                mine = shared_memory.SharedMemory(create=True, size=int(n) * 8)
+                names = [None] * self.world
+                self.dist.all_gather_object(names, mine.name)
+                maps = [mine if nm == mine.name else shared_memory.SharedMemory(name=nm) for nm in names]
+                self._shm = getattr(self, "_shm", []) + [(mine, maps)]
+                arrays = [np.ndarray((int(n),), dtype=np.float64, buffer=m.buf) for m in maps]
+                return [torch.from_numpy(arrays[self.ranks[0]])], [arrays]
+
+            def barrier(self):
+                self.dist.barrier()
+
+            def close(self):
+                self.dist.barrier()
+                for mine, maps in getattr(self, "_shm", []):
+                    for m in maps:
+                        if m is not mine:
+                            m.close()
+                    mine.close()
+                    mine.unlink()
+                self._shm = []
+
+        return _Shm(*a, **k)

@@ -2,8 +2,10 @@
 
 Two processes run the sharded gram / residual / synthesis of
 paper_2502_04217_b200.sharded with a NumPy shard backend (tests/helpers) and
-compare each rank's slab with the oracle on the full grid; also checks the
-all-reduce combiners.  The CUDA shard kernels are checked on the GPU by
+compare each rank's slab with the oracle on the full grid, for both slab
+exchanges: all-to-all, and the peer-store exchange (shared-memory buffers
+standing in for the CUDA IPC allocations; same barrier placement); also
+checks the all-reduce combiners.  The CUDA shard kernels are checked on the GPU by
 tests/test_gpu_sharded.py (emulated ranks).
 """
 
@@ -35,8 +37,11 @@ def test_sharded_transforms_world_size_2():
     assert proc.returncode == 0, proc.stderr[-3000:]
     line = next(l for l in proc.stdout.splitlines() if l.startswith("RESULT "))
     res = json.loads(line[len("RESULT "):])
-    assert len(res) == 3
+    assert len(res) == 9  # 3 grids x (all-to-all, peer exchange, peer == all-to-all)
     for dims, r in res.items():
+        if dims.endswith("peer==a2a"):
+            assert r is True, dims  # the peer-store exchange is bitwise the all-to-all one
+            continue
         assert r["gram"] <= 1e-12, (dims, r)
         assert r["resid"] <= 1e-12, (dims, r)
         assert r["synth"] <= 1e-12, (dims, r)
