@@ -843,6 +843,17 @@ Entry make(int kind, bool epi) {
   if constexpr (M <= 512) {
     if (light) return make_cfg<M, S, kCfgLight>(kind, epi);
   }
+  if constexpr (M >= 1024) {
+    // long fibres (E = 16): the fibre tiles fill one CTA per SM anyway (one
+    // staged tile is 138 KB), so ask for one and let the FFT keep ~200
+    // registers: 1024^3 gram 37.2 -> 33.1 ms, 2048^2 0.115 -> 0.100 ms.
+    // FL_CFG_BIG = 1 (256 threads, no staging, 2 CTAs/SM) / 2 (512 threads,
+    // no staging) / 0 (the m <= 512 heavy variant) for comparison.
+    static const int big = env_cfg("FL_CFG_BIG");
+    if (big == 1) return make_cfg<M, S, cfg_code(0, 0, 2)>(kind, epi);
+    if (big == 2) return make_cfg<M, S, cfg_code(1, 0, 1)>(kind, epi);
+    if (big != 0) return make_cfg<M, S, cfg_code(0, 1, 1)>(kind, epi);
+  }
   return make_cfg<M, S, kCfgHeavy>(kind, epi);
 }
 

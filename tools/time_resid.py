@@ -1,6 +1,6 @@
-"""Time fl_residual_adjoint (5-pass A^T Z (b_hat - A beta)) and fl_gram at side^3.
+"""Time fl_residual_adjoint (A^T Z (b_hat - A beta)) and fl_gram at side^3 or --dims.
 
-    python tools/time_resid.py [--size 512] [--reps 10]
+    python tools/time_resid.py [--size 512 | --dims 2048,2048] [--reps 10]
 """
 import argparse
 import os
@@ -17,12 +17,21 @@ from paper_2502_04217_b200 import _dev, _lib, workloads  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--size", type=int, default=512)
+    ap.add_argument("--dims", default=None, help="e.g. 2048,2048 (random 15%% mask)")
     ap.add_argument("--reps", type=int, default=10)
     args = ap.parse_args()
-    side = args.size
-    n = side ** 3
-    shape = fl.GridShape((side,) * 3)
-    mask = fl.Mask.from_bool(workloads.bragg_flags(side), shape)
+    if args.dims:
+        import numpy as np
+
+        dims = tuple(int(d) for d in args.dims.split(","))
+        shape = fl.GridShape(dims)
+        n = shape.n
+        mask = fl.Mask.from_bool(np.random.default_rng(0).random(n) < 0.15, shape)
+    else:
+        side = args.size
+        n = side ** 3
+        shape = fl.GridShape((side,) * 3)
+        mask = fl.Mask.from_bool(workloads.bragg_flags(side), shape)
     dm = mask.on_device()
     plan = _dev.plan_for(shape.dims)
     g = torch.Generator(device="cuda").manual_seed(0)
