@@ -43,8 +43,9 @@ struct MGeom {
 
 __device__ __forceinline__ int own(int q, int b, int nb) { return b == 0 ? q : (q == 0 ? nb / 2 : nb - q); }
 
-// One radix-8 stage on both butterflies (twiddles from the length-M table).
-template <int M, int S>
+// One radix-8 stage on both butterflies (twiddles from a length-TM table,
+// TM = M normally; TM = 2M when the length-M FFT is a half of a 2M one).
+template <int M, int S, int TM = M>
 __device__ __forceinline__ void stage(double2* v, int q, const double2* tw, int sign) {
   using G = MGeom<M>;
   constexpr int NS = G::ns(S);
@@ -55,7 +56,7 @@ __device__ __forceinline__ void stage(double2* v, int q, const double2* tw, int 
       const int qq = own(q, b, G::NB);
       const int j = qq % NS;
       double2 w[8];
-      fast::twiddles<M, 8, NS>(w, j, tw, sign);
+      fast::twiddles<TM, 8, NS>(w, j, tw, sign);
 #pragma unroll
       for (int s = 1; s < 8; ++s) u[s] = cmul(u[s], w[s]);
     }
@@ -93,12 +94,12 @@ __device__ __forceinline__ void exchange(double2* v, double2* fib, int q) {
   __syncthreads();
 }
 
-template <int M, int S = 0>
+template <int M, int S = 0, int TM = M>
 __device__ __forceinline__ void fft(double2* v, double2* fib, int q, const double2* tw, int sign) {
-  stage<M, S>(v, q, tw, sign);
+  stage<M, S, TM>(v, q, tw, sign);
   if constexpr (S + 1 < MGeom<M>::NST) {
     exchange<M, S>(v, fib, q);
-    fft<M, S + 1>(v, fib, q, tw, sign);
+    fft<M, S + 1, TM>(v, fib, q, tw, sign);
   }
 }
 

@@ -161,7 +161,8 @@ def test_interior_violation_raises():
         ns.barrier_diagonals(s, s, bad, s)
 
 
-@pytest.mark.parametrize("dims", [(256, 256, 256), (2048, 2048), (512, 64, 64), (8192, 256)])
+@pytest.mark.parametrize("dims", [(256, 256, 256), (2048, 2048), (512, 64, 64), (8192, 256),
+                                  (1024, 64, 32), (16, 1024, 48), (1024, 1024), (1030, 40, 16)])
 def test_large_grid_matches_oracle(dims):
     """Full-size grids (hundreds of tiles per persistent CTA) against the oracle.
 

@@ -116,3 +116,26 @@ print("ok")
     env = dict(os.environ, FL_FUSED_EPI="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("split", ["0", "2"])
+def test_split_1024_engine_matches_oracle(split):
+    """Strided m = 1024 passes with and without the radix-2 split into two
+    mirrored 512-point halves (FL_SPLIT is read once per process)."""
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2502_04217_b200 as fl
+from oracle import fftlasso_oracle as orc
+rng = np.random.default_rng(11)
+for dims in [(1024, 8, 16), (8, 1024, 24), (1024, 1024)]:
+    beta = rng.standard_normal(int(np.prod(dims)))
+    tol = 1e-12 * np.abs(beta).max()
+    sh = fl.GridShape(dims)
+    assert np.max(np.abs(fl.synthesize(beta, sh) - orc.synthesize(beta, dims))) <= tol, dims
+    assert np.max(np.abs(fl.analyze(beta, sh) - orc.analyze(beta, dims))) <= tol, dims
+print("OK")
+''' % REPO
+    env = dict(os.environ, FL_SPLIT=split)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
