@@ -147,6 +147,13 @@ FL_API int fl_slab_unpack_x(int64_t a, int64_t d1, int64_t d2, int nranks, const
  * observed count through ``n_observed`` (synchronises). */
 FL_API int fl_mask_build(int64_t n, const uint8_t* flags, uint32_t* miss_bits, int64_t* obs_offsets,
                   int64_t* n_observed, fl_stream_t stream);
+/* On-device input generation: the Bragg-peak punch mask
+ * of the C3-C5 recipes -- voxel missing when the summed squared periodic
+ * distances to the nearest multiple of ``spacing`` along every axis are
+ * <= radius^2 (bitwise equal to fl_mask_build of the host formula) -- built
+ * straight into bits + observed offsets, no host flags.  Synchronises. */
+FL_API int fl_mask_bragg(int ndim, const int64_t* dims, int64_t spacing, double radius, uint32_t* miss_bits,
+                         int64_t* offsets, int64_t* n_observed, fl_stream_t stream);
 /* embed (masking.py:90-99): full = 0; full[observed] = obs. */
 FL_API int fl_embed(int64_t n, const uint32_t* miss_bits, const int64_t* obs_offsets,
              const double* obs, double* full, fl_stream_t stream);

@@ -97,6 +97,7 @@ SIGNATURES = {
     "fl_ftb_ratio": (_I, [_I64, _P, _P, ctypes.POINTER(_D), _P]),
     "fl_axpy": (_I, [_I64, _D, _P, _P, _P]),
     "fl_xpby": (_I, [_I64, _P, _D, _P, _P]),
+    "fl_mask_bragg": (_I, [_I, ctypes.POINTER(_I64), _I64, _D, _P, _P, ctypes.POINTER(_I64), _P]),
     "fl_soft_threshold": (_I, [_I64, _P, _D, _P, _P]),
     "fl_slab_x_to_y_peers": (_I, [_I64, _I64, _I64, _I, _I, _P, ctypes.POINTER(_P), _P]),
     "fl_slab_y_to_x_peers": (_I, [_I64, _I64, _I64, _I, _I, _P, ctypes.POINTER(_P), _P]),

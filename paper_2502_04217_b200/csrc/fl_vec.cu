@@ -63,6 +63,41 @@ __global__ void k_mask_bits(int64_t n, const uint8_t* __restrict__ flags, uint32
   }
 }
 
+// Bragg-peak punch (workloads.bragg_flags): voxel missing when the summed
+// squared periodic distances to the nearest multiple of `spacing` along every
+// axis are <= r2.  Integer distances, compared in double as NumPy does.
+__global__ void k_bragg_bits(int64_t n, int ndim, int64_t d1, int64_t d2, int64_t sp, double r2,
+                             uint32_t* __restrict__ bits, int64_t* __restrict__ counts) {
+  const int64_t nw = (n + 31) >> 5;
+  GRID_LOOP(w, nw) {
+    uint32_t word = 0;
+    int valid = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t v = (w << 5) + b;
+      if (v >= n) break;
+      ++valid;
+      int64_t rem = v, sum = 0;
+      const int64_t ext[2] = {d2, d1};
+      for (int a = 0; a < ndim; ++a) {  // innermost axis first
+        int64_t t;
+        if (a < ndim - 1) {
+          const int64_t e = ext[a];
+          t = rem % e;
+          rem /= e;
+        } else {
+          t = rem;
+        }
+        t %= sp;
+        const int64_t m = t < sp - t ? t : sp - t;
+        sum += m * m;
+      }
+      if ((double)sum <= r2) word |= 1u << b;
+    }
+    bits[w] = word;
+    counts[w] = valid - __popc(word);
+  }
+}
+
 __device__ __forceinline__ int64_t obs_slot(const uint32_t* bits, const int64_t* off, int64_t v,
                                             bool& miss) {
   const uint32_t word = bits[v >> 5];
@@ -822,13 +857,9 @@ using namespace fl;
 
 extern "C" {
 
-int fl_mask_build(int64_t n, const uint8_t* flags, uint32_t* bits, int64_t* offsets,
-                  int64_t* n_observed, fl_stream_t stream) {
-  if (n <= 0 || !flags || !bits || !offsets) return fail(FL_E_VALUE, "bad mask arguments");
-  cudaStream_t s = (cudaStream_t)stream;
-  const int64_t nw = (n + 31) >> 5;
-  k_mask_bits<<<grid_for(nw, T, 1 << 16), T, 0, s>>>(n, flags, bits, offsets);
-  FL_LAUNCH_CHECK();
+// offsets[w] = observed samples before word w (exclusive scan of the
+// per-word observed counts already in `offsets`); *n_observed = total.
+static int mask_offsets(int64_t nw, int64_t* offsets, int64_t* n_observed, cudaStream_t s) {
   int64_t last_count = 0;
   FL_CUDA(cudaMemcpyAsync(&last_count, offsets + nw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   size_t tmp_bytes = 0;
@@ -843,6 +874,32 @@ int fl_mask_build(int64_t n, const uint8_t* flags, uint32_t* bits, int64_t* offs
   FL_CUDA(cudaStreamSynchronize(s));
   if (n_observed) *n_observed = last_off + last_count;
   return FL_OK;
+}
+
+int fl_mask_build(int64_t n, const uint8_t* flags, uint32_t* bits, int64_t* offsets,
+                  int64_t* n_observed, fl_stream_t stream) {
+  if (n <= 0 || !flags || !bits || !offsets) return fail(FL_E_VALUE, "bad mask arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nw = (n + 31) >> 5;
+  k_mask_bits<<<grid_for(nw, T, 1 << 16), T, 0, s>>>(n, flags, bits, offsets);
+  FL_LAUNCH_CHECK();
+  return mask_offsets(nw, offsets, n_observed, s);
+}
+
+int fl_mask_bragg(int ndim, const int64_t* dims, int64_t spacing, double radius, uint32_t* bits,
+                  int64_t* offsets, int64_t* n_observed, fl_stream_t stream) {
+  if (ndim < 1 || ndim > 3 || !dims || spacing < 1 || !bits || !offsets) return fail(FL_E_VALUE, "bad mask arguments");
+  int64_t n = 1;
+  for (int a = 0; a < ndim; ++a) {
+    if (dims[a] < 1) return fail(FL_E_SHAPE, "bad grid extent");
+    n *= dims[a];
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nw = (n + 31) >> 5;
+  const int64_t d2 = dims[ndim - 1], d1 = ndim >= 2 ? dims[ndim - 2] : 1;
+  k_bragg_bits<<<grid_for(nw, T, 1 << 16), T, 0, s>>>(n, ndim, d1, d2, spacing, radius * radius, bits, offsets);
+  FL_LAUNCH_CHECK();
+  return mask_offsets(nw, offsets, n_observed, s);
 }
 
 int fl_embed(int64_t n, const uint32_t* bits, const int64_t* off, const double* obs, double* full,

@@ -19,7 +19,7 @@ from . import _dev, _lib
 from .errors import UnsupportedShapeError
 from .fourier import GridShape
 
-__all__ = ["Mask", "observe", "observe_adjoint", "gram", "embed", "restrict"]
+__all__ = ["Mask", "BraggMask", "observe", "observe_adjoint", "gram", "embed", "restrict"]
 
 
 class DeviceMask:
@@ -89,6 +89,62 @@ class Mask:
             dm = DeviceMask(self)
             self._dev_cache[dev.index] = dm
         return dm
+
+
+class BraggMask:
+    """The Bragg-peak punch mask of the C3-C5 recipes, generated on the GPU.
+
+    Same missing set as ``Mask.from_bool(workloads.bragg_flags(...), shape)``
+    (bit for bit), built straight into the device bitmask and observed
+    offsets (``fl_mask_bragg``) -- no n-byte host flags, no index array, so a
+    C5-sized problem needs no host-side mask at all.
+    Usable wherever the solver takes a ``Mask``; ``missing`` /
+    ``missing_bool`` are materialised on the host only if asked for.
+    """
+
+    def __init__(self, shape: GridShape, spacing: int = 16, radius: float = 5.3):
+        import torch
+
+        self.shape = shape
+        dev = _dev.device()
+        nw = (shape.n + 31) // 32
+        bits = torch.empty(nw, dtype=torch.int32, device=dev)
+        offsets = torch.empty(nw, dtype=torch.int64, device=dev)
+        dims = (ctypes.c_int64 * shape.ndim)(*shape.dims)
+        n_obs = ctypes.c_int64()
+        _lib.call("fl_mask_bragg", shape.ndim, dims, int(spacing), float(radius), _dev.ptr(bits),
+                  _dev.ptr(offsets), ctypes.byref(n_obs), _dev.stream())
+        if n_obs.value <= 0:
+            raise ValueError("cannot mask every sample")
+        dm = DeviceMask.__new__(DeviceMask)
+        dm.bits, dm.offsets, dm.n_observed, dm.device = bits, offsets, n_obs.value, dev
+        self._dm = dm
+        self._host = None
+
+    @property
+    def n_observed(self) -> int:
+        return self._dm.n_observed
+
+    @property
+    def n_missing(self) -> int:
+        return self.shape.n - self._dm.n_observed
+
+    def on_device(self) -> DeviceMask:
+        if _dev.device() != self._dm.device:
+            raise ValueError("BraggMask lives on the device it was built on")
+        return self._dm
+
+    @property
+    def missing_bool(self) -> np.ndarray:
+        if self._host is None:
+            words = self._dm.bits.cpu().numpy().view(np.uint32)
+            flags = np.unpackbits(words.view(np.uint8), bitorder="little")[: self.shape.n].astype(bool)
+            self._host = flags
+        return self._host
+
+    @property
+    def missing(self) -> np.ndarray:
+        return np.flatnonzero(self.missing_bool)
 
 
 def _coeffs(beta, mask: Mask):

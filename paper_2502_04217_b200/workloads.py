@@ -109,6 +109,39 @@ def c4_const(n_side: int) -> Instance:
     return Instance((n_side,) * 3, beta, flags, 0.05 * rng.standard_normal(n_obs), 0.5)
 
 
+def c4_const_device(n_side: int, noise_seed: int = 0):
+    """C4/C5 recipe generated on the GPU -> (mask, b, beta_idx, beta_val, lam).
+
+    The Bragg mask is built on the device (``masking.BraggMask``, bit-equal
+    to ``bragg_flags``); the spikes are c4_const's own (same host RNG stream,
+    only n/10^4 positions); the observation noise is drawn on the device with
+    torch's Philox generator, so ``b`` is NOT NumPy-identical to c4_const --
+    a C5-scale input without any n-sized host array.
+    """
+    import torch
+
+    from . import _dev
+    from .fourier import GridShape, synthesize
+    from .masking import BraggMask, restrict
+
+    shape = GridShape((n_side,) * 3)
+    n = shape.n
+    rng = np.random.default_rng(1234)
+    nnz = max(8, n // 10000)
+    idx = rng.choice(n, nnz, replace=False)
+    val = rng.uniform(1, 2, nnz) * rng.choice([-1., 1.], nnz)
+    mask = BraggMask(shape)
+    beta = torch.zeros(n, dtype=torch.float64, device=_dev.device())
+    beta[torch.from_numpy(idx).to(beta.device)] = torch.from_numpy(val).to(beta.device)
+    x = synthesize(beta, shape)
+    del beta
+    b = restrict(x, mask)
+    del x
+    g = torch.Generator(device=b.device).manual_seed(noise_seed)
+    b += 0.05 * torch.randn(b.numel(), dtype=torch.float64, device=b.device, generator=g)
+    return mask, b, idx, val, 0.5
+
+
 def harmonics(dims, noise_seed: int = 0, missing_fraction: float = 0.15,
               missing_seed: int = 1):
     """Reference generator (synthetic.py:32-63): product-of-harmonics truth.

@@ -243,3 +243,40 @@ def test_large_download_ring_exact(rng):
     h = _dev.out(t, True)
     assert isinstance(h, np.ndarray) and h.shape == (n,)
     assert h.tobytes() == t.cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("dims", [(64, 64, 64), (96, 64, 32), (48, 80), (4096,)])
+def test_bragg_mask_on_device_equals_host_formula(dims):
+    """fl_mask_bragg == fl_mask_build(bragg flags): same bits, offsets, counts,
+    and a solve with either mask is bitwise the same."""
+    from paper_2502_04217_b200.masking import BraggMask
+
+    shape = fl.GridShape(dims)
+    grids = np.meshgrid(*[np.arange(d) % 16 for d in dims], indexing="ij")
+    dist = sum(np.minimum(t, 16 - t).astype(np.int64) ** 2 for t in grids)
+    flags = (dist <= 5.3 * 5.3).reshape(-1)
+    host = fl.Mask.from_bool(flags, shape)
+    dev = BraggMask(shape)
+    hd, dd = host.on_device(), dev.on_device()
+    assert dev.n_missing == host.n_missing
+    assert dd.bits.cpu().numpy().tobytes() == hd.bits.cpu().numpy().tobytes()
+    assert dd.offsets.cpu().numpy().tobytes() == hd.offsets.cpu().numpy().tobytes()
+    np.testing.assert_array_equal(dev.missing, host.missing)
+    if len(dims) == 3:
+        b = np.random.default_rng(3).standard_normal(host.n_observed)
+        r1 = fl.solve(b, host, fl.IpmConfig(lam=0.5, max_iters=3))
+        r2 = fl.solve(b, dev, fl.IpmConfig(lam=0.5, max_iters=3))
+        assert r1[0].tobytes() == r2[0].tobytes() and r1[1].krylov_counts == r2[1].krylov_counts
+
+
+def test_c4_recipe_generated_on_device():
+    from paper_2502_04217_b200 import workloads
+
+    mask, b, idx, val, lam = workloads.c4_const_device(64)
+    inst = workloads.c4_const(64)
+    np.testing.assert_array_equal(np.flatnonzero(inst.beta_true), np.sort(idx))
+    assert b.is_cuda and b.numel() == mask.n_observed == int((~inst.flags).sum())
+    beta, rep = fl.solve(b, mask, fl.IpmConfig(lam=lam))
+    assert rep.converged
+    found = np.flatnonzero(np.abs(beta.cpu().numpy()) > 1e-6 * float(beta.abs().max()))
+    np.testing.assert_array_equal(found, np.sort(idx))
