@@ -308,6 +308,12 @@ FL_API int fl_slab_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int nranks, i
                                 double* const* y_slabs, fl_stream_t stream);
 FL_API int fl_slab_y_to_x_peers(int64_t a, int64_t b, int64_t d2, int nranks, int rank, const double* y_slab,
                                 double* const* x_slabs, fl_stream_t stream);
+/* The X->Y exchange of planes [i0_begin, i0_begin + i0_count) of this rank's
+ * slab (``x_planes`` points at plane i0_begin): lets the exchange of one
+ * chunk of planes run while the next chunk is still being transformed. */
+FL_API int fl_slab_x_to_y_peers_planes(int64_t a, int64_t d1, int64_t d2, int nranks, int rank,
+                                       int64_t i0_begin, int64_t i0_count, const double* x_planes,
+                                       double* const* y_slabs, fl_stream_t stream);
 /* cudaMalloc + cudaIpcGetMemHandle (64-byte handle), the peer side's open /
  * close, and the matching free. */
 FL_API int fl_ipc_alloc(int64_t bytes, void** ptr, unsigned char* handle64);

@@ -101,6 +101,7 @@ SIGNATURES = {
     "fl_soft_threshold": (_I, [_I64, _P, _D, _P, _P]),
     "fl_slab_x_to_y_peers": (_I, [_I64, _I64, _I64, _I, _I, _P, ctypes.POINTER(_P), _P]),
     "fl_slab_y_to_x_peers": (_I, [_I64, _I64, _I64, _I, _I, _P, ctypes.POINTER(_P), _P]),
+    "fl_slab_x_to_y_peers_planes": (_I, [_I64, _I64, _I64, _I, _I, _I64, _I64, _P, ctypes.POINTER(_P), _P]),
     "fl_ipc_alloc": (_I, [_I64, ctypes.POINTER(_P), ctypes.c_char_p]),
     "fl_ipc_open": (_I, [ctypes.c_char_p, ctypes.POINTER(_P)]),
     "fl_ipc_close": (_I, [_P]),

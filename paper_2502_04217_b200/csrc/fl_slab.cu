@@ -95,11 +95,12 @@ struct Peers {
 // X-slab (a, d1, d2) of rank `me` -> Y-slabs (b, d2, d0) of every rank:
 //   Y[j / b][((j % b) d2 + i2) d0 + me a + i0] = x[(i0 d1 + j) d2 + i2]
 // One CTA per (j, 32x32 tile of (i0, i2)).
+// (ac planes starting at plane i0off of the slab: the chunked, overlapped form)
 __global__ void k_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int P, int me, const double* __restrict__ x,
-                               Peers dst) {
+                               Peers dst, int64_t ac, int64_t i0off) {
   __shared__ double tile[32][33];
   const int64_t b = d1 / P, d0 = a * P;
-  const int64_t t0 = (a + 31) / 32, t2 = (d2 + 31) / 32;
+  const int64_t t0 = (ac + 31) / 32, t2 = (d2 + 31) / 32;
   int64_t id = blockIdx.x;
   const int64_t ti2 = id % t2;
   id /= t2;
@@ -109,14 +110,14 @@ __global__ void k_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int P, int me,
   const int64_t base0 = ti0 * 32, base2 = ti2 * 32;
   for (int k = ty; k < 32; k += 8) {  // read: i2 fastest
     const int64_t i0 = base0 + k, i2 = base2 + tx;
-    if (i0 < a && i2 < d2) tile[k][tx] = x[(i0 * d1 + j) * d2 + i2];
+    if (i0 < ac && i2 < d2) tile[k][tx] = x[(i0 * d1 + j) * d2 + i2];
   }
   __syncthreads();
   double* y = dst.p[j / b];
   const int64_t j1 = j % b;
   for (int k = ty; k < 32; k += 8) {  // write: i0 fastest
     const int64_t i2 = base2 + k, i0 = base0 + tx;
-    if (i0 < a && i2 < d2) y[(j1 * d2 + i2) * d0 + me * a + i0] = tile[tx][k];
+    if (i0 < ac && i2 < d2) y[(j1 * d2 + i2) * d0 + me * a + i0off + i0] = tile[tx][k];
   }
 }
 
@@ -208,18 +209,26 @@ int fl_slab_pack_y(int64_t a, int64_t b, int64_t d2, int nranks, const double* y
   return y_blocks(false, a, b, d2, nranks, y_slab, send, (cudaStream_t)stream);
 }
 
-int fl_slab_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int nranks, int rank, const double* x_slab,
-                         double* const* y_slabs, fl_stream_t stream) {
-  if (!x_slab || !y_slabs) return fail(FL_E_VALUE, "null argument");
+int fl_slab_x_to_y_peers_planes(int64_t a, int64_t d1, int64_t d2, int nranks, int rank, int64_t i0_begin,
+                                int64_t i0_count, const double* x_planes, double* const* y_slabs,
+                                fl_stream_t stream) {
+  if (!x_planes || !y_slabs) return fail(FL_E_VALUE, "null argument");
   if (nranks < 1 || d1 % nranks || rank < 0 || rank >= nranks) return fail(FL_E_SHAPE, "bad slab geometry");
+  if (i0_begin < 0 || i0_count < 0 || i0_begin + i0_count > a) return fail(FL_E_SHAPE, "plane range outside the slab");
   Peers pe;
   FL_TRY(peers_of(nranks, y_slabs, &pe));
-  const int64_t blocks = d1 * ((a + 31) / 32) * ((d2 + 31) / 32);
+  const int64_t blocks = d1 * ((i0_count + 31) / 32) * ((d2 + 31) / 32);
   if (blocks > 0x7fffffffLL) return fail(FL_E_SHAPE, "slab too large");
   if (blocks == 0) return FL_OK;
-  k_x_to_y_peers<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a, d1, d2, nranks, rank, x_slab, pe);
+  k_x_to_y_peers<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a, d1, d2, nranks, rank, x_planes, pe,
+                                                                       i0_count, i0_begin);
   FL_LAUNCH_CHECK();
   return FL_OK;
+}
+
+int fl_slab_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int nranks, int rank, const double* x_slab,
+                         double* const* y_slabs, fl_stream_t stream) {
+  return fl_slab_x_to_y_peers_planes(a, d1, d2, nranks, rank, 0, a, x_slab, y_slabs, stream);
 }
 
 int fl_slab_y_to_x_peers(int64_t a, int64_t b, int64_t d2, int nranks, int rank, const double* y_slab,

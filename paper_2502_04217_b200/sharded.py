@@ -267,10 +267,11 @@ class ShardOps:
         return torch.from_numpy(pack_bits(flags)).to(_dev.device())
 
     def close(self):
-        for h in (self.x_plan, self.y_plan):
+        for h in (self.x_plan, self.y_plan, *self.__dict__.get("_chunk_plans", {}).values()):
             if h:
                 _lib.lib().fl_plan_destroy(h)
         self.x_plan = self.y_plan = None
+        self.__dict__.pop("_chunk_plans", None)
 
     def synth_x(self, src, dst):  # axes 2 then 1 of the X-slab
         _lib.call("fl_axis_pass", self.x_plan, 2, 0, _dev.ptr(src), _dev.ptr(dst), _dev.stream())
@@ -304,6 +305,26 @@ class ShardOps:
     def unpack_x(self, recv, x):
         g = self.geo
         _lib.call("fl_slab_unpack_x", g.a, g.dims[1], g.dims[2], g.P, _dev.ptr(recv), _dev.ptr(x), _dev.stream())
+
+    def synth_x_planes(self, src, dst, i0, count):
+        """synth_x on planes [i0, i0 + count) only (for the overlapped exchange)."""
+        g = self.geo
+        key = int(count)
+        plans = self.__dict__.setdefault("_chunk_plans", {})
+        if key not in plans:
+            plans[key] = self._plan((key, g.dims[1], g.dims[2]), 0b110, _dev.device().index)
+        off = int(i0) * g.dims[1] * g.dims[2] * 8
+        s_ = ctypes.c_void_p(src.data_ptr() + off)
+        d_ = ctypes.c_void_p(dst.data_ptr() + off)
+        _lib.call("fl_axis_pass", plans[key], 2, 0, s_, d_, _dev.stream())
+        _lib.call("fl_axis_pass", plans[key], 1, 0, d_, d_, _dev.stream())
+
+    def x_to_y_peers_planes(self, rank, x, table, i0, count):
+        g = self.geo
+        off = int(i0) * g.dims[1] * g.dims[2] * 8
+        _lib.call("fl_slab_x_to_y_peers_planes", g.a, g.dims[1], g.dims[2], g.P, rank, int(i0), int(count),
+                  ctypes.c_void_p(x.data_ptr() + off), ctypes.cast(table, ctypes.POINTER(ctypes.c_void_p)),
+                  _dev.stream())
 
     def x_to_y_peers(self, rank, x, table):
         g = self.geo
@@ -379,6 +400,43 @@ class ShardedGrid:
             op.unpack_x(rv, x)
         return xs
 
+    def _overlapped_forward(self, betas, outs) -> bool:
+        """synth_x + X->Y exchange in plane chunks, the exchange of chunk c on a
+        side stream while chunk c+1 is transformed (peer exchange only).
+
+        Default: 4 chunks with two or more ranks (the NVLink stores overlap the
+        next chunk's passes); off for one rank / LocalComm, where both compete
+        for the same SMs and HBM (measured: 194 -> 187 matvecs/s at 512^3, P = 1).
+        ``FL_SHARD_CHUNKS`` overrides; the chunked path is tested in emulation.
+        """
+        import os
+
+        K = int(os.environ.get("FL_SHARD_CHUNKS", "4" if isinstance(self.comm, DistComm) and self.comm.world > 1 else "1"))
+        a = self.geo.a
+        if self.exchange != "peer" or K <= 1 or a % K or not hasattr(self.ops[0], "synth_x_planes"):
+            return False
+        import torch
+
+        main = torch.cuda.current_stream()
+        side = self.__dict__.get("_xstream")
+        if side is None:
+            side = self._xstream = torch.cuda.Stream(main.device)
+        side.wait_stream(main)
+        ac = a // K
+        for i, (op, r, b, o) in enumerate(zip(self.ops, self.comm.ranks, betas, outs)):
+            for c in range(K):
+                op.synth_x_planes(b, o, c * ac, ac)
+                ev = torch.cuda.Event()
+                ev.record(main)
+                side.wait_event(ev)
+                with torch.cuda.stream(side):
+                    op.x_to_y_peers_planes(r, o, self.ytab[i], c * ac, ac)
+        main.wait_stream(side)
+        for o in outs:
+            o.record_stream(side)
+        self.comm.barrier()
+        return True
+
     def synthesize_to_y(self, betas, ys):
         """A beta with beta in X-slabs; result in Y-slabs (b, d2, d0)."""
         scratch = self.xrecv if self.exchange == "peer" else self.ybuf
@@ -393,9 +451,10 @@ class ShardedGrid:
 
         Returns the all-reduced ||Z A beta||^2 when ``want_norm`` (gram only).
         """
-        for op, b, o in zip(self.ops, betas, outs):
-            op.synth_x(b, o)
-        self.x_to_y(outs, self.ybuf)
+        if not self._overlapped_forward(betas, outs):
+            for op, b, o in zip(self.ops, betas, outs):
+                op.synth_x(b, o)
+            self.x_to_y(outs, self.ybuf)
         norms = []
         for i, (op, y) in enumerate(zip(self.ops, self.ybuf)):
             norms.append(op.fused_y(bits_y[i], None if bhat_y is None else bhat_y[i], y, y, want_norm))

@@ -119,3 +119,22 @@ def test_sharded_solve_peer_exchange_equals_a2a():
         betas, rep = sh.sharded_solve(prob, lam, fl.IpmConfig(lam=lam))
         res[ex] = (rep.krylov_counts, rep.final_objective, b"".join(t.cpu().numpy().tobytes() for t in betas))
     assert res["a2a"] == res["peer"]
+
+
+def test_overlapped_forward_exchange_bitwise(monkeypatch):
+    """synth_x + X->Y exchange in plane chunks on two streams == one shot."""
+    dims = (64, 32, 48)
+    out = {}
+    for k in ("1", "4"):
+        monkeypatch.setenv("FL_SHARD_CHUNKS", k)
+        comm = sh.LocalComm(2)
+        grid = sh.ShardedGrid(dims, comm, exchange="peer")
+        geo = grid.geo
+        beta = np.random.default_rng(5).standard_normal(geo.n)
+        flags = np.random.default_rng(6).random(geo.n) < 0.15
+        prob = sh.ShardedProblem.from_host(grid, flags, np.where(flags, 0.0, 1.0))
+        xb = [fl._dev.to_dev(geo.x_slab(beta, r)) for r in comm.ranks]
+        g = [fl._dev.empty(geo.n_local) for _ in comm.ranks]
+        nrm = grid.gram(xb, g, prob.bits_y, want_norm=True)
+        out[k] = (nrm, b"".join(t.cpu().numpy().tobytes() for t in g))
+    assert out["1"] == out["4"]
