@@ -138,3 +138,32 @@ def test_overlapped_forward_exchange_bitwise(monkeypatch):
         nrm = grid.gram(xb, g, prob.bits_y, want_norm=True)
         out[k] = (nrm, b"".join(t.cpu().numpy().tobytes() for t in g))
     assert out["1"] == out["4"]
+
+
+def test_sharded_solve_8_ranks_c4_recipe_64():
+    """The C5 configuration's rank count (P = 8, peer exchange, chunked
+    forward overlap forced on) on the C4 recipe at 64^3 against the
+    single-GPU solve."""
+    import os
+
+    from paper_2502_04217_b200 import workloads
+
+    inst = workloads.c4_const(64)
+    shape = fl.GridShape(inst.dims)
+    mask = fl.Mask.from_bool(inst.flags, shape)
+    b = fl.observe(inst.beta_true, mask) + inst.noise
+    beta1, rep1 = fl.solve(b, mask, fl.IpmConfig(lam=inst.lam))
+    os.environ["FL_SHARD_CHUNKS"] = "2"
+    try:
+        grid = sh.ShardedGrid(inst.dims, sh.LocalComm(8), exchange="peer")
+        bhat = np.zeros(shape.n)
+        bhat[~inst.flags] = b
+        prob = sh.ShardedProblem.from_host(grid, inst.flags, bhat)
+        betas, rep = sh.sharded_solve(prob, inst.lam, fl.IpmConfig(lam=inst.lam))
+    finally:
+        del os.environ["FL_SHARD_CHUNKS"]
+    beta = grid.geo.from_x([t.cpu().numpy() for t in betas])
+    assert rep.status == rep1.status == "converged" and rep.iterations == rep1.iterations
+    assert all(abs(x - y) <= 1 for x, y in zip(rep.krylov_counts, rep1.krylov_counts))
+    assert abs(rep.final_objective - rep1.final_objective) <= 1e-9 * abs(rep1.final_objective)
+    assert np.linalg.norm(beta - beta1) <= 1e-8 * np.linalg.norm(beta1)
