@@ -59,7 +59,7 @@ def test_dense_equivalence(dims):
     assert np.max(np.abs(a.T - at_fast)) <= 1e-12
 
 
-@pytest.mark.parametrize("dims", [(4,), (4096,), (32, 32, 32), (64, 64), (2, 2), (128, 96, 64),
+@pytest.mark.parametrize("dims", [(4,), (4096,), (1 << 20,), (2, 1 << 16), (16384, 6), (32, 32, 32), (64, 64), (2, 2), (128, 96, 64),
                                   (2048, 2048), (256, 256, 256)])
 def test_orthogonality_and_isometry(dims, rng):
     shape = fl.GridShape(dims)
@@ -162,7 +162,7 @@ def test_interior_violation_raises():
 
 
 @pytest.mark.parametrize("dims", [(256, 256, 256), (2048, 2048), (512, 64, 64), (8192, 256),
-                                  (1024, 64, 32), (16, 1024, 48), (1024, 1024), (1030, 40, 16)])
+                                  (1024, 64, 32), (16, 1024, 48), (1024, 1024), (1030, 40, 16), (1 << 20,), (4, 1 << 16)])
 def test_large_grid_matches_oracle(dims):
     """Full-size grids (hundreds of tiles per persistent CTA) against the oracle.
 
