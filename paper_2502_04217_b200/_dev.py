@@ -121,7 +121,7 @@ def zeros(n: int):
     return torch.zeros(int(n), dtype=F64, device=device())
 
 
-_DOWNLOAD_RING_MIN = 1 << 30
+_DOWNLOAD_RING_MIN = 4 << 30
 
 
 def out(t, like_host: bool):
@@ -129,7 +129,7 @@ def out(t, like_host: bool):
 
     The device->host copy lands in page-locked memory from torch's caching
     host allocator (full-bandwidth DMA; freed results are recycled by later
-    calls), exposed to the caller as a NumPy view.  Results of 1 GiB and
+    calls), exposed to the caller as a NumPy view.  Results of 4 GiB and
     more go through a ring of pinned 64 MiB chunks into an ordinary NumPy
     array instead (pinning many GB per call costs seconds).
     """

@@ -232,12 +232,14 @@ def test_large_numpy_upload_exact(rng):
 
 
 def test_large_download_ring_exact(rng):
-    """Results >= 1 GiB come back through the pinned ring into a NumPy array."""
+    """Results >= 4 GiB come back through the pinned ring into a NumPy array."""
     import torch
 
     from paper_2502_04217_b200 import _dev
 
-    n = (1 << 27) + 10  # 1 GiB + 80 B: ragged last chunk
+    from paper_2502_04217_b200 import _dev as d_
+
+    n = (d_._DOWNLOAD_RING_MIN >> 3) + 10  # threshold + 80 B: ragged last chunk
     g = torch.Generator(device="cuda").manual_seed(7)
     t = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
     h = _dev.out(t, True)
