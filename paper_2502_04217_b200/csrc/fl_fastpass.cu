@@ -1,6 +1,8 @@
 // Dispatcher of the register-resident pass kernels (templates in
 // fl_fastpass.cuh).  The per-length instantiations live in fl_fp_small.cu,
 // fl_fp_512.cu and fl_fp_large.cu so they compile in parallel.
+#include <cstdlib>
+
 #include "fl_fastpass.cuh"
 
 namespace fl {
@@ -16,6 +18,7 @@ Entry make_1024(bool strided, int kind, bool epi);
 Entry make_2048(bool strided, int kind, bool epi);
 Entry make_4096(bool strided, int kind, bool epi);
 Entry make_8192(bool strided, int kind, bool epi);
+Entry make_split_1024(int kind);
 
 Entry lookup(int m, bool strided, int kind, bool epi) {
   switch (m) {
@@ -64,7 +67,18 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
   // persistent grid size per kernel variant (resident CTAs x SMs)
   static std::mutex mu;
   static std::unordered_map<const void*, int> grids;
-  Entry e = lookup(m, strided, kind, epi);
+  // strided m = 1024 synthesis / analysis: the radix-2 split into two mirrored
+  // 512-point halves (fl_split.cuh) wins on the large-stride axis (1024^3
+  // axis 0: synthesis 7.44 -> 6.36 ms, analysis 7.43 -> 6.18 ms) and loses on
+  // the 8 KiB-stride one (4.98 -> 5.94 ms), so it is chosen by stride.
+  // FL_SPLIT = 0 never, 2 always, default by stride.
+  static const int split_mode = [] {
+    const char* v = std::getenv("FL_SPLIT");
+    return v ? std::atoi(v) : 1;
+  }();
+  const bool split = m == 1024 && strided && !epi && (kind == K_SYNTH || kind == K_ANALYZE) &&
+                     (split_mode == 2 || (split_mode == 1 && A.inner >= 16384));
+  Entry e = split ? fpk::make_split_1024(kind) : lookup(m, strided, kind, epi);
   if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");
   int grid_cap = 0;
   {

@@ -818,23 +818,6 @@ inline int mirror_mode() {
 template <int M, bool S>
 Entry make(int kind, bool epi) {
   const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE || kind == K_COPY);
-  if constexpr (M == 1024 && S) {
-    // strided m = 1024 analysis: radix-2 split into two mirrored 512-point
-    // halves (fl_split.cuh); FL_SPLIT=0 keeps the E = 16 engine, FL_SPLIT=2
-    // also splits the synthesis (measured slower on axis 1)
-    static const int sp = [] {
-      const char* e = std::getenv("FL_SPLIT");
-      return e ? std::atoi(e) : 1;
-    }();
-    if (sp && !epi && (kind == K_ANALYZE || (sp == 2 && kind == K_SYNTH))) {
-      Entry e;
-      e.fn = kind == K_SYNTH ? split::split_pass<K_SYNTH> : split::split_pass<K_ANALYZE>;
-      e.threads = split::T;
-      e.smem = split::SMEM;
-      e.w = split::W;
-      return e;
-    }
-  }
   if constexpr (M == 64 || M == 512 || M == 4096) {
     int mm = kind == K_COPY ? 0 : mirror_mode();
     if ((mm == 5 || mm == 6) && !light && (kind == K_GRAM || kind == K_RESID)) {

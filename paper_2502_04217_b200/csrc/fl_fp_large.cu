@@ -9,5 +9,16 @@ Entry make_2048(bool strided, int kind, bool epi) { return make_any<2048>(stride
 Entry make_4096(bool strided, int kind, bool epi) { return make_any<4096>(strided, kind, epi); }
 Entry make_8192(bool strided, int kind, bool epi) { return make_any<8192>(strided, kind, epi); }
 
+// strided m = 1024 as two mirrored 512-point halves (fl_split.cuh)
+Entry make_split_1024(int kind) {
+  Entry e;
+  if (kind == K_SYNTH) e.fn = split::split_pass<K_SYNTH>;
+  else if (kind == K_ANALYZE) e.fn = split::split_pass<K_ANALYZE>;
+  e.threads = split::T;
+  e.smem = split::SMEM;
+  e.w = split::W;
+  return e;
+}
+
 }  // namespace fpk
 }  // namespace fl

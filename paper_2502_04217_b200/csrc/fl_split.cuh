@@ -77,8 +77,36 @@ __global__ void __launch_bounds__(T, 1) split_pass(const PassArgs A) {
     const Geo Q = geo<true>(A, valid ? g : 0);
     double2 v[16];
     if constexpr (KIND == K_SYNTH) {
+      if (h == 0) {
+        // even spectrum: slot j holds Zin_{2j}, its mirror slot 512 - j holds
+        // Zin_{1024-2j} -- one read of rows (2j+1, 2j+512) serves both (the
+        // mirrored unpack of fl_fastpass.cuh with k = 2j); q = 0 owns Z_0, Z_H
+        const double c0 = A.c0, c1 = A.c1;
+        constexpr int NB = G::NB;
+        const int jb1 = q0 ? NB / 2 : NB - q;
+        constexpr int GEN[8] = {15, 14, 13, 12, 4, 5, 6, 7};
+        constexpr int Q0[8] = {4, 7, 6, 5, 12, 13, 14, 15};
+        fast::static_for<0, 8>([&](auto I) {
+          constexpr int i = decltype(I)::value;
+          const int j = i < 4 ? q + i * NB : jb1 + (7 - i) * NB;  // 512-space index, j < 256
+          const bool sp = i == 0 && q0;
+          const double2 a = row(A, Q, valid, sp ? 0 : 2 * j + 1);
+          const double2 bb = row(A, Q, valid, sp ? 1 : 2 * j + H);
+          double2 l = make_double2(c1 * (a.x - bb.y), c1 * (bb.x + a.y));  // Zin_{2j}
+          double2 hh = make_double2(c1 * (a.x + bb.y), c1 * (a.y - bb.x));  // Zin_{1024-2j}
+          if constexpr (i == 0) {
+            l = sp ? make_double2(c0 * a.x, c0 * a.y) : l;
+            hh = sp ? make_double2(c0 * bb.x, c0 * bb.y) : hh;
+          }
+          if constexpr (i < 4) v[i] = l;
+          else v[15 - i] = l;
+          v[GEN[i]] = q0 ? v[GEN[i]] : hh;
+          v[Q0[i]] = q0 ? hh : v[Q0[i]];
+        });
+      } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = zin(A, Q, valid, 2 * mirror::slot_k<512>(q, i >> 3, i & 7) + h);
+        for (int i = 0; i < 16; ++i) v[i] = zin(A, Q, valid, 2 * mirror::slot_k<512>(q, i >> 3, i & 7) + 1);
+      }
       mirror::fft<512, 0, 1024>(v, fib, q, tw, +1);
       // radix-2 combine: swap E / O between the halves through shared memory
 #pragma unroll
