@@ -216,6 +216,18 @@ class DistComm(Comm):
         return [_wrap_device(ptr.value, n)], [table]
 
 
+    def release_peer_buffers(self):
+        """Close the peers' IPC mappings and free this rank's exchange buffers
+        (collective: every rank calls it once it is done with the grid)."""
+        self.dist.barrier(group=self.group)
+        for ptr in getattr(self, "_opened", []):
+            _lib.call("fl_ipc_close", ctypes.c_void_p(ptr))
+        self.dist.barrier(group=self.group)
+        for ptr in getattr(self, "_owned", []):
+            _lib.call("fl_dev_free", ctypes.c_void_p(ptr))
+        self._opened, self._owned = [], []
+
+
 class _CudaArray:
     """__cuda_array_interface__ view of a raw device allocation (for torch.as_tensor)."""
 
