@@ -371,7 +371,7 @@ class ShardedGrid:
             try:
                 self.ybuf, self.ytab = comm.peer_buffers(n)
                 self.xrecv, self.xtab = comm.peer_buffers(n)
-            except (RuntimeError, OSError, ValueError, AttributeError) as exc:
+            except (RuntimeError, OSError, ValueError, AttributeError, MemoryError) as exc:
                 if exchange == "peer":  # explicitly requested: do not hide the failure
                     raise
                 import warnings
