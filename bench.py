@@ -630,7 +630,7 @@ def main():
                 "clocks": res["clocks"], "gpu_launches": res["launches"],
             }
             print(json.dumps(line), flush=True)
-        if world > 1:
+        if dist.is_available() and dist.is_initialized():
             dist.barrier()
             dist.destroy_process_group()
         return

@@ -192,29 +192,52 @@ class DistComm(Comm):
         self.dist.all_reduce(t, group=self.group)
 
     def peer_buffers(self, n):
+        """Collective and all-or-nothing: every rank allocates, the handles are
+        all-gathered, every rank opens every peer's buffer; if any rank fails
+        at any step, all ranks raise (so they fall back together)."""
         import torch
 
+        dev = self.device if self.device is not None else "cpu"
         ptr = ctypes.c_void_p()
         handle = ctypes.create_string_buffer(64)
-        _lib.call("fl_ipc_alloc", n * 8, ctypes.byref(ptr), handle)
-        mine = torch.frombuffer(bytearray(handle.raw), dtype=torch.uint8)
-        dev = self.device if self.device is not None else "cpu"
-        gathered = [torch.empty(64, dtype=torch.uint8, device=dev) for _ in range(self.world)]
-        self.dist.all_gather(gathered, mine.to(dev), group=self.group)
+        ok = 1
+        try:
+            _lib.call("fl_ipc_alloc", n * 8, ctypes.byref(ptr), handle)
+        except (RuntimeError, MemoryError, OSError):
+            ok = 0
+        mine = torch.frombuffer(bytearray(handle.raw + bytes([ok])), dtype=torch.uint8).to(dev)
+        gathered = [torch.empty(65, dtype=torch.uint8, device=dev) for _ in range(self.world)]
+        self.dist.all_gather(gathered, mine, group=self.group)
+        got = [g.cpu().numpy().tobytes() for g in gathered]
         me = self.ranks[0]
-        ptrs = []
-        for r, h in enumerate(gathered):
-            if r == me:
-                ptrs.append(ptr.value)
-                continue
-            q = ctypes.c_void_p()
-            _lib.call("fl_ipc_open", bytes(h.cpu().numpy().tobytes()), ctypes.byref(q))
-            ptrs.append(q.value)
-            self._opened = getattr(self, "_opened", []) + [q.value]
+        ptrs, opened = [], []
+        if all(g[64] == 1 for g in got):
+            for r, g in enumerate(got):
+                if r == me:
+                    ptrs.append(ptr.value)
+                    continue
+                q = ctypes.c_void_p()
+                try:
+                    _lib.call("fl_ipc_open", g[:64], ctypes.byref(q))
+                except (RuntimeError, OSError):
+                    ok = 0
+                    break
+                ptrs.append(q.value)
+                opened.append(q.value)
+        else:
+            ok = 0
+        flag = torch.tensor([float(ok)], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
+        if flag.item() < 1.0:
+            for q in opened:
+                _lib.call("fl_ipc_close", ctypes.c_void_p(q))
+            if ptr.value:
+                _lib.call("fl_dev_free", ptr)
+            raise RuntimeError("peer buffers unavailable on at least one rank")
+        self._opened = getattr(self, "_opened", []) + opened
         self._owned = getattr(self, "_owned", []) + [ptr.value]
         table = (ctypes.c_void_p * self.world)(*ptrs)
         return [_wrap_device(ptr.value, n)], [table]
-
 
     def release_peer_buffers(self):
         """Close the peers' IPC mappings and free this rank's exchange buffers
