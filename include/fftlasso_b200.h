@@ -333,6 +333,22 @@ FL_API int fl_ipm_newton_pcg(fl_plan_t plan, const uint32_t* miss_bits, const fl
                              double abs_tol, double rel_tol, int64_t max_iters, fl_pcg_result* res,
                              fl_stream_t stream);
 
+/* One IPM step (ipm.py:364-394, the fused form of newton_direction +
+ * fraction_to_boundary + the state update) with no host sync after the PCG
+ * start: fl_ipm_newton_pcg, then the ratio minima, the step lengths
+ * alpha = min(1, tau * ratio) on the device, the state update (skipped when
+ * the PCG did not converge or alpha < 1e-12) and the interior flag.  The
+ * verdict lands in pinned ``host_out`` (13 doubles: ratio minima[4], alpha_p,
+ * alpha_d, skipped, interior flag, PCG status 1 converged / 2 cap /
+ * 3 curvature / 4 r'P^{-1}r breakdown, PCG iterations, residual norm,
+ * offending value, initial norm) after the caller's next stream sync.  The
+ * same kernels in the same order as fl_ipm_newton_pcg + fl_ipm_ratios +
+ * fl_ipm_update, so the iterates are bitwise those of that path. */
+FL_API int fl_ipm_newton_step(fl_plan_t plan, const uint32_t* miss_bits, const fl_state* st, const double* g,
+                              double lam, double mu, double tau, double* sigma1, double* sigma2, double* x,
+                              double* work, double abs_tol, double rel_tol, int64_t max_iters, double* host_out,
+                              fl_stream_t stream);
+
 /* ---- diagnostics (diagnostics.py) -------------------------------------- */
 /* out = sign(x) * max(|x| - t, 0) elementwise, NumPy conventions
  * (soft_threshold, diagnostics.py:325-328); in place allowed. */

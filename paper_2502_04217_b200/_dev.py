@@ -117,6 +117,11 @@ def empty(n: int):
     return torch.empty(int(n), dtype=F64, device=device())
 
 
+def pinned(n: int):
+    """Page-locked host doubles (targets of asynchronous device->host copies)."""
+    return torch.zeros(int(n), dtype=F64, pin_memory=True)
+
+
 def zeros(n: int):
     return torch.zeros(int(n), dtype=F64, device=device())
 

@@ -78,6 +78,8 @@ SIGNATURES = {
     "fl_pcg_kkt": (_I, [_P] * 7 + [_D, _D, _I64, ctypes.POINTER(FlPcgResult), _P, _I64, _P]),
     "fl_ipm_newton_pcg": (_I, [_P, _P, ctypes.POINTER(FlState), _P, _D, _D, _P, _P, _P, _P, _D, _D, _I64,
                                ctypes.POINTER(FlPcgResult), _P]),
+    "fl_ipm_newton_step": (_I, [_P, _P, ctypes.POINTER(FlState), _P, _D, _D, _D, _P, _P, _P, _P, _D, _D, _I64,
+                                _P, _P]),
     "fl_pcg_step_init": (_I, [_I64] + [_P] * 6 + [ctypes.POINTER(_D), _P]),
     "fl_pcg_step_update": (_I, [_I64, _P, _P, _D, _P, _P, _P, _P, ctypes.POINTER(_D), _P]),
     "fl_pcg_step_pupdate": (_I, [_I64, _P, _P, _P, _D, _P, ctypes.POINTER(_D), _P]),

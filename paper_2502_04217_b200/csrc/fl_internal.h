@@ -81,6 +81,9 @@ int pcg_pupdate(int64_t n, const double* sig1, const double* sig2, const double*
 // restructured PCG: curvature = ||Z A p_beta||^2 (fused gram pass) + diagonal form
 int pcg2_init(int64_t n, const double* sig1, const double* sig2, const double* rhs, double* x, double* r,
               double* p, double* partials, int* nblocks, cudaStream_t s);
+int ipm_step_device(int64_t n, const fl_state* st, const double* sigma1, const double* sigma2, double mu,
+                    double tau, const double* d_beta, const double* d_z, const int* pcg_status, double* dev,
+                    cudaStream_t s);
 int pcg2_update(int64_t n, const double* sig1, const double* sig2, const double* rho, const double* curv_g,
                 const double* curv_d, double* x, double* r, const double* p, const double* gp,
                 double* partials, int* nblocks, cudaStream_t s);

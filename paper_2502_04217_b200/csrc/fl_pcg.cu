@@ -206,6 +206,16 @@ __global__ void k_pcg_control(PcgCtl* __restrict__ c, double* __restrict__ slots
   }
 }
 
+// PCG verdict into the step record (fl_ipm_newton_step): dev[8..12].
+__global__ void k_step_pack(const PcgCtl* __restrict__ c, double norm0, double* __restrict__ dev) {
+  if (threadIdx.x != 0) return;
+  dev[8] = (double)c->status;
+  dev[9] = (double)c->k;
+  dev[10] = c->norm;
+  dev[11] = c->bad;
+  dev[12] = norm0;
+}
+
 struct PcgGraph {
   const uint32_t* bits;
   const double *sig1, *sig2;
@@ -481,6 +491,62 @@ int fl_ipm_newton_pcg(fl_plan_t p, const uint32_t* bits, const fl_state* st, con
   if (pcg_mode() == 3)
     return pcg_v3_loop(p, bits, sigma1, sigma2, x, work, rho, abs_tol, rel_tol, limit, res, s);
   return pcg_v2_loop(p, bits, sigma1, sigma2, x, work, rho, abs_tol, rel_tol, limit, res, nullptr, 0, s);
+}
+
+
+// One IPM step with a single host sync before the loop's convergence check
+// (ipm.py:364-394): newton_setup + PCG as fl_ipm_newton_pcg, then ratios,
+// device step lengths, the gated state update and the interior flag
+// (ipm_step_device), and ONE asynchronous copy of the step verdict to
+// ``host_out`` (13 doubles, pinned): [0..3] ratio minima, [4] alpha_p,
+// [5] alpha_d, [6] skipped, [7] interior flag, [8] PCG status (1 converged,
+// 2 iteration cap, 3 curvature breakdown, 4 r'P^{-1}r breakdown), [9] PCG
+// iterations, [10] residual norm, [11] offending value, [12] initial norm.
+// Valid after the caller's next stream sync (fl_ipm_assess).
+int fl_ipm_newton_step(fl_plan_t p, const uint32_t* bits, const fl_state* st, const double* g, double lam,
+                       double mu, double tau, double* sigma1, double* sigma2, double* x, double* work,
+                       double abs_tol, double rel_tol, int64_t max_iters, double* host_out, fl_stream_t stream) {
+  if (!p || !bits || !st || !g || !sigma1 || !sigma2 || !x || !work || !host_out)
+    return fail(FL_E_VALUE, "null argument");
+  if (abs_tol < 0 || rel_tol < 0) return fail(FL_E_VALUE, "tolerances must be nonnegative");
+  if (abs_tol == 0 && rel_tol == 0) return fail(FL_E_VALUE, "abs_tol and rel_tol cannot both be zero");
+  const int64_t n = p->n;
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  int nb = 0;
+  double rho = 0.0, flag = 0.0;
+  FL_TRY(newton_setup(n, st, g, lam, mu, sigma1, sigma2, x, work, work + 2 * n, sc->partials, &nb, s));
+  FL_TRY(pcg_start_fetch(sc, nb, true, work + 6 * n, &rho, &flag, s));
+  if (flag != 0.0) return fail(FL_E_INTERIOR, "slacks and multipliers must be strictly positive and finite");
+  FL_TRY(check_rho(rho, 0));
+  const int64_t limit = pcg_limit(n, max_iters);
+  double* slots = work + 6 * n;
+  PcgCtl* ctl = reinterpret_cast<PcgCtl*>(slots + 8);
+  PcgCtl* hc = reinterpret_cast<PcgCtl*>(sc->host);
+  const double norm0 = std::sqrt(rho);
+  const double thr = abs_tol + rel_tol * norm0;
+  if (norm0 <= thr || limit <= 0) {
+    *hc = PcgCtl{thr, norm0, 0.0, (long long)limit, 0, norm0 <= thr ? 1 : 2, 1};
+    FL_CUDA(cudaMemcpyAsync(ctl, hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
+  } else if (pcg_mode() == 3) {
+    cudaGraphExec_t exec;
+    FL_TRY(pcg_graph(p, bits, sigma1, sigma2, x, work, &exec));
+    *hc = PcgCtl{thr, norm0, 0.0, (long long)limit, 0, 0, 0};
+    FL_CUDA(cudaMemcpyAsync(ctl, hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
+    FL_CUDA(cudaGraphLaunch(exec, s));
+  } else {
+    fl_pcg_result r{};
+    FL_TRY(pcg_v2_loop(p, bits, sigma1, sigma2, x, work, rho, abs_tol, rel_tol, limit, &r, nullptr, 0, s));
+    *hc = PcgCtl{thr, r.residual_norm, 0.0, (long long)limit, (long long)r.iterations, r.converged ? 1 : 2, 1};
+    FL_CUDA(cudaMemcpyAsync(ctl, hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
+  }
+  double* dev = sc->result + 32;
+  FL_TRY(ipm_step_device(n, st, sigma1, sigma2, mu, tau, x, x + n, &ctl->status, dev, s));
+  k_step_pack<<<1, 32, 0, s>>>(ctl, norm0, dev);
+  FL_LAUNCH_CHECK();
+  FL_CUDA(cudaMemcpyAsync(host_out, dev, 13 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  return FL_OK;
 }
 
 }  // extern "C"

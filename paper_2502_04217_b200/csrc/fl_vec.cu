@@ -297,10 +297,16 @@ __device__ __forceinline__ double step(double v, double a, double dv) { return a
 __global__ void k_update(int64_t n, fl_state st, const double* __restrict__ sig1,
                          const double* __restrict__ sig2, double mu, const double* __restrict__ db,
                          const double* __restrict__ dz, double ap, double ad,
-                         double* __restrict__ partials) {
+                         double* __restrict__ partials, const double* __restrict__ alpha_dev = nullptr) {
   __shared__ double red[32];
   double flag = 0.0;
-  GRID_LOOP(i, n) {
+  // device step lengths (k_step_alpha): [alpha_p, alpha_d, skip]
+  const bool skip = alpha_dev && alpha_dev[2] != 0.0;
+  if (alpha_dev) {
+    ap = alpha_dev[0];
+    ad = alpha_dev[1];
+  }
+  if (!skip) GRID_LOOP(i, n) {
     LOAD_STATE(i)
     const double b = db[i], c = dz[i];
     const Dir d = direction(beta, z, s1, s2, y1, y2, nu1, nu2, sig1[i], sig2[i], mu, b, c);
@@ -317,6 +323,28 @@ __global__ void k_update(int64_t n, fl_state st, const double* __restrict__ sig1
     if (n1 <= 0.0 || n2 <= 0.0 || n3 <= 0.0 || n4 <= 0.0) flag = 1.0;
   }
   emit(flag, MaxOp(), red, partials, 0);
+}
+
+// Step lengths on the device from the four ratio minima (ipm.py:355-361):
+// the same IEEE operations as ipm._alpha_from_ratio and Python's min() on the
+// host (min(a, b) keeps a unless b < a).  skip = 1 when the PCG verdict is not
+// "converged" or the step collapsed (< 1e-12): the gated update then leaves
+// the state untouched and the host raises after its one sync.
+__device__ __forceinline__ double alpha_of(double ratio, double tau) {
+  if (ratio == INFINITY) return 1.0;
+  const double a = tau * ratio;
+  return a < 1.0 ? a : 1.0;
+}
+__device__ __forceinline__ double pymin(double a, double b) { return b < a ? b : a; }
+
+__global__ void k_step_alpha(const double* __restrict__ minima, const int* __restrict__ pcg_status,
+                             double tau, double* __restrict__ alpha) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double ap = pymin(alpha_of(minima[0], tau), alpha_of(minima[1], tau));
+  const double ad = pymin(alpha_of(minima[2], tau), alpha_of(minima[3], tau));
+  alpha[0] = ap;
+  alpha[1] = ad;
+  alpha[2] = (*pcg_status != 1 || pymin(ap, ad) < 1e-12) ? 1.0 : 0.0;
 }
 
 __global__ void k_update_explicit(int64_t n, fl_state st, fl_state dir, double ap, double ad,
@@ -849,6 +877,27 @@ int pcg_pupdate(int64_t n, const double* sig1, const double* sig2, const double*
   k_pcg_pupdate<<<grid_for(n, T), T, 0, s>>>(n, sig1, sig2, r, beta, p);
   FL_LAUNCH_CHECK();
   return FL_OK;
+}
+
+// Back half of the IPM step with no host sync (ipm.py:364-394): ratio minima
+// -> dev[0..3], step lengths -> dev[4..6] (gated on *pcg_status), the state
+// update, interior flag -> dev[7].
+int ipm_step_device(int64_t n, const fl_state* st, const double* sigma1, const double* sigma2, double mu,
+                    double tau, const double* d_beta, const double* d_z, const int* pcg_status, double* dev,
+                    cudaStream_t s) {
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  const int grid = grid_for(n, T);
+  k_ratios<<<grid, T, 0, s>>>(n, *st, sigma1, sigma2, mu, d_beta, d_z, sc->partials);
+  FL_LAUNCH_CHECK();
+  const int kinds[4] = {RED_MIN, RED_MIN, RED_MIN, RED_MIN};
+  FL_TRY(finish_reduce(sc->partials, grid, 4, kinds, dev, s));
+  k_step_alpha<<<1, 32, 0, s>>>(dev, pcg_status, tau, dev + 4);
+  FL_LAUNCH_CHECK();
+  k_update<<<grid, T, 0, s>>>(n, *st, sigma1, sigma2, mu, d_beta, d_z, 0.0, 0.0, sc->partials, dev + 4);
+  FL_LAUNCH_CHECK();
+  const int kind = RED_MAX;
+  return finish_reduce(sc->partials, grid, 1, &kind, dev + 7, s);
 }
 
 }  // namespace fl

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import time
 from dataclasses import dataclass
 
@@ -447,6 +448,7 @@ class Workspace:
         self.g = self.work[4 * n:5 * n]
         self.best_beta = _dev.empty(n)
         self.fs = fl_state(self.state)
+        self.verdict = _dev.pinned(16)  # fl_ipm_newton_step's step record
 
 
 def _fused_step(prob: Problem, ws: Workspace, mu: float, lam: float, config: IpmConfig):
@@ -481,6 +483,47 @@ def _fused_step(prob: Problem, ws: Workspace, mu: float, lam: float, config: Ipm
             f"fraction-to-boundary step collapsed (alpha_p={alpha_p:.2e}, alpha_d={alpha_d:.2e})")
     _lib.call("fl_ipm_update", n, ctypes.byref(ws.fs), _dev.ptr(ws.sig1), _dev.ptr(ws.sig2),
               float(mu), db, dz, float(alpha_p), float(alpha_d), s)
+    return res, alpha_p, alpha_d
+
+
+# FL_IPM_ASYNC=0 selects the step with a host sync after each stage
+# (_fused_step); the default issues the whole step with one sync (the
+# assessment's), same kernels in the same order, bitwise the same iterates.
+_ASYNC_STEP = os.environ.get("FL_IPM_ASYNC", "1") != "0"
+
+
+def _launch_step(prob: Problem, ws: Workspace, mu: float, lam: float, config: IpmConfig) -> None:
+    """ipm_step (ipm.py:364-394) issued without waiting: PCG, step lengths and
+    the state update run on the device; the verdict lands in ``ws.verdict``."""
+    n = prob.n
+    pc = _pcg_config(config)
+    tau = max(config.ftb_tau, 1.0 - mu)
+    _lib.call("fl_ipm_newton_step", prob.plan.handle, _dev.ptr(prob.dmask.bits), ctypes.byref(ws.fs),
+              _dev.ptr(ws.g), float(lam), float(mu), float(tau), _dev.ptr(ws.sig1), _dev.ptr(ws.sig2),
+              _dev.ptr(ws.x), _dev.ptr(ws.work), float(pc.abs_tol), float(pc.rel_tol),
+              int(pc.iteration_limit(2 * n)), ws.verdict.data_ptr(), _dev.stream())
+
+
+def _step_verdict(ws: Workspace):
+    """Read the step record after the stream synchronised; raise as the
+    synchronous path would (PCG breakdown / stall, collapsed step, interior)."""
+    v = ws.verdict.tolist()
+    status, k = int(v[8]), int(v[9])
+    if status == 3:
+        raise NumericalBreakdownError(f"nonpositive curvature p'Kp = {v[11]:f} at iteration {k}")
+    if status == 4:
+        raise NumericalBreakdownError(f"r'P^{{-1}}r = {v[11]:f} at iteration {k}")
+    res = PcgResult(ws.x, k, status == 1, float(v[10]), None)
+    if not res.converged:
+        raise NumericalBreakdownError(
+            f"PCG stalled at preconditioned residual {res.residual_norm:.3e} "
+            f"after {res.iterations} iterations")
+    alpha_p, alpha_d = v[4], v[5]
+    if min(alpha_p, alpha_d) < 1e-12:
+        raise StalledError(
+            f"fraction-to-boundary step collapsed (alpha_p={alpha_p:.2e}, alpha_d={alpha_d:.2e})")
+    if v[7] != 0.0:
+        raise StalledError("slack or multiplier left the strict interior")
     return res, alpha_p, alpha_d
 
 
@@ -523,9 +566,15 @@ def solve(b, mask: Mask, config: IpmConfig = IpmConfig(),
             st.mu = next_barrier(st.mu, config.tol, config)
 
         t_iter = time.perf_counter()
-        res, alpha_p, alpha_d = _fused_step(prob, ws, st.mu, lam, config)
-        prob.residual_adjoint(st.beta, ws.g)
-        a = prob.assess(st, ws.g, lam, st.mu)
+        if _ASYNC_STEP:
+            _launch_step(prob, ws, st.mu, lam, config)
+            prob.residual_adjoint(st.beta, ws.g)
+            a = prob.assess(st, ws.g, lam, st.mu)
+            res, alpha_p, alpha_d = _step_verdict(ws)
+        else:
+            res, alpha_p, alpha_d = _fused_step(prob, ws, st.mu, lam, config)
+            prob.residual_adjoint(st.beta, ws.g)
+            a = prob.assess(st, ws.g, lam, st.mu)
         conv = _conv_report(a, n, config.tol, config.gamma_centrality)
         record = IterationRecord(
             iteration=iteration,

@@ -362,3 +362,72 @@ def test_fused_newton_front_half_bitwise():
             _lib.call("fl_ipm_newton_pcg", prob.plan.handle, _dev.ptr(prob.dmask.bits), ctypes.byref(fsb),
                       _dev.ptr(gv), lam, mu, _dev.ptr(s1), _dev.ptr(s2), _dev.ptr(x), _dev.ptr(work),
                       1e-12, 0.0, 5000, ctypes.byref(out), _dev.stream())
+
+
+def test_one_sync_step_bitwise_equals_synchronous_step():
+    """FL_IPM_ASYNC=1 (default: fl_ipm_newton_step, step lengths and the gated
+    update on the device, one host sync per IPM iteration) == FL_IPM_ASYNC=0
+    (a sync after the PCG, the ratios and the update): identical records and
+    bitwise identical solutions, with the graph PCG loop and the host loop."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    code = r'''
+import sys, json, hashlib, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_2502_04217_b200 as fl
+from conftest import load_golden
+out = {}
+for name in ("c1_4096", "c2_256", "c3_32", "harm_16", "empty_128", "maxit_64"):
+    g = load_golden("solve_" + name)
+    dims = tuple(int(d) for d in g["dims"])
+    mi = 3 if name == "maxit_64" else 200
+    beta, rep = fl.solve(g["b"], fl.Mask(g["missing"], fl.GridShape(dims)),
+                         fl.IpmConfig(lam=float(g["lam"]), max_iters=mi))
+    recs = [[r.mu, r.alpha_primal, r.alpha_dual, r.krylov_iters, r.pcg_residual, r.kkt_max]
+            for r in rep.records]
+    out[name] = [rep.status, recs, rep.final_objective, hashlib.sha1(beta.tobytes()).hexdigest()]
+print(json.dumps(out))
+''' % (REPO, REPO + "/tests")
+    res = {}
+    for mode in ("0", "1"):
+        for pcg in ("2", "3"):
+            env = dict(os.environ, FL_IPM_ASYNC=mode, FL_PCG=pcg)
+            out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                                 timeout=600)
+            assert out.returncode == 0, out.stderr[-2000:]
+            res[mode + pcg] = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["03"] == res["13"] == res["02"] == res["12"]
+
+
+def test_one_sync_step_cap_skips_update():
+    """A PCG that hits its iteration cap: fl_ipm_newton_step leaves the state
+    untouched (gated update) and the verdict says status 2 / skipped; the
+    solver raises NumericalBreakdownError as the synchronous path does."""
+    import ctypes
+
+    from paper_2502_04217_b200 import _dev, _lib
+
+    g = load_golden("solve_c1_4096")
+    dims = tuple(int(d) for d in g["dims"])
+    mask = fl.Mask(g["missing"], fl.GridShape(dims))
+    lam = float(g["lam"])
+    n = mask.shape.n
+    ws = ipm.Workspace(n)
+    prob = ipm.Problem(g["b"], mask, scratch=ws.work)
+    _lib.call("fl_ipm_init", n, ctypes.byref(ws.fs), lam, _dev.stream())
+    before = [getattr(ws.state, f).cpu().numpy().tobytes() for f in ipm.FIELDS]
+    prob.residual_adjoint(ws.state.beta, ws.g)
+    _lib.call("fl_ipm_newton_step", prob.plan.handle, _dev.ptr(prob.dmask.bits), ctypes.byref(ws.fs),
+              _dev.ptr(ws.g), lam, lam / 2, 0.995, _dev.ptr(ws.sig1), _dev.ptr(ws.sig2), _dev.ptr(ws.x),
+              _dev.ptr(ws.work), 1e-30, 0.0, 2, ws.verdict.data_ptr(), _dev.stream())
+    import torch
+    torch.cuda.synchronize()
+    v = ws.verdict.tolist()
+    assert v[8] == 2 and v[9] == 2 and v[6] == 1.0
+    assert [getattr(ws.state, f).cpu().numpy().tobytes() for f in ipm.FIELDS] == before
+    with pytest.raises(fl.NumericalBreakdownError, match="PCG stalled"):
+        ipm._step_verdict(ws)
