@@ -162,8 +162,11 @@ struct PcgCtl {      // at work + 6n + 8 (8 doubles)
   double bad;        // offending value of a breakdown
   long long limit;   // iteration cap
   long long k;       // iterations done
-  int status;        // 0 running, 1 converged, 2 cap reached, 3 curvature, 4 r'P^{-1}r breakdown
+  int status;        // 0 running, 1 converged, 2 cap reached, 3 curvature, 4 r'P^{-1}r breakdown,
+                     // 5 non-interior state (gated graph only)
   int done;
+  double abs_tol;    // gated graph: thr is formed on the device from these
+  double rel_tol;
 };
 static_assert(sizeof(PcgCtl) <= 8 * sizeof(double), "PcgCtl must fit its work slots");
 
@@ -206,6 +209,41 @@ __global__ void k_pcg_control(PcgCtl* __restrict__ c, double* __restrict__ slots
   }
 }
 
+// Gate ahead of the WHILE node (gated graph of fl_ipm_newton_step): the PCG
+// start check done on the device instead of pcg_start_fetch's host sync --
+// res = reduced start partials [rho, diagonal curvature, interior flag].
+// Same tests in the same order as the host (interior flag, r'P^{-1}r, then
+// ||r0|| <= thr), thr = abs_tol + rel_tol * sqrt(rho) rounded as on the host
+// (no contraction).  Opens the loop only when there is work to do.
+__global__ void k_pcg_gate(PcgCtl* __restrict__ c, const double* __restrict__ res, double* __restrict__ slots,
+                           double* __restrict__ dev, cudaGraphConditionalHandle h) {
+  if (threadIdx.x != 0) return;
+  const double rho = res[0];
+  slots[0] = rho;
+  slots[3] = res[1];
+  int st = 0;
+  double bad = 0.0;
+  dev[12] = NAN;
+  if (res[2] != 0.0) {
+    st = 5;
+  } else if (!isfinite(rho) || rho < 0) {
+    st = 4;
+    bad = rho;
+  } else {
+    const double norm0 = sqrt(rho);
+    dev[12] = norm0;
+    c->norm = norm0;
+    c->thr = __dadd_rn(c->abs_tol, __dmul_rn(c->rel_tol, norm0));
+    if (norm0 <= c->thr) st = 1;
+    else if (c->limit <= 0) st = 2;
+  }
+  c->k = 0;
+  c->bad = bad;
+  c->status = st;
+  c->done = st != 0;
+  cudaGraphSetConditional(h, st == 0 ? 1 : 0);
+}
+
 // PCG verdict into the step record (fl_ipm_newton_step): dev[8..12].
 __global__ void k_step_pack(const PcgCtl* __restrict__ c, double norm0, double* __restrict__ dev) {
   if (threadIdx.x != 0) return;
@@ -213,13 +251,14 @@ __global__ void k_step_pack(const PcgCtl* __restrict__ c, double norm0, double* 
   dev[9] = (double)c->k;
   dev[10] = c->norm;
   dev[11] = c->bad;
-  dev[12] = norm0;
+  if (norm0 >= 0.0) dev[12] = norm0;  // < 0: written by the gate
 }
 
 struct PcgGraph {
   const uint32_t* bits;
   const double *sig1, *sig2;
   double *x, *work;
+  bool gated;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
@@ -256,29 +295,47 @@ int enqueue_iteration(fl_plan_t p, const uint32_t* bits, const double* sigma1, c
 }
 
 int pcg_graph(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, double* x,
-              double* work, cudaGraphExec_t* out) {
+              double* work, cudaGraphExec_t* out, bool gated = false) {
   auto* gs = static_cast<PcgGraphs*>(p->pcg_graphs);
   if (!gs) {
     gs = new PcgGraphs();
     p->pcg_graphs = gs;
   }
   for (const PcgGraph& g : gs->v)
-    if (g.bits == bits && g.sig1 == sigma1 && g.sig2 == sigma2 && g.x == x && g.work == work) {
+    if (g.bits == bits && g.sig1 == sigma1 && g.sig2 == sigma2 && g.x == x && g.work == work &&
+        g.gated == gated) {
       *out = g.exec;
       return FL_OK;
     }
   if (!gs->capture) FL_CUDA(cudaStreamCreateWithFlags(&gs->capture, cudaStreamNonBlocking));
-  PcgGraph g{bits, sigma1, sigma2, x, work};
+  PcgGraph g{bits, sigma1, sigma2, x, work, gated};
   FL_CUDA(cudaGraphCreate(&g.graph, 0));
   cudaGraphConditionalHandle h;
-  FL_CUDA(cudaGraphConditionalHandleCreate(&h, g.graph, 1, cudaGraphCondAssignDefault));
+  // gated: the loop starts closed and k_pcg_gate opens it
+  FL_CUDA(cudaGraphConditionalHandleCreate(&h, g.graph, gated ? 0 : 1, cudaGraphCondAssignDefault));
+  cudaGraphNode_t gate = nullptr;
+  if (gated) {
+    Scratch* sc;
+    FL_TRY(scratch(&sc));
+    PcgCtl* ctl = reinterpret_cast<PcgCtl*>(work + 6 * p->n + 8);
+    const double* res = sc->result;
+    double* slots = work + 6 * p->n;
+    double* dev = sc->result + 32;
+    void* args[] = {&ctl, &res, &slots, &dev, &h};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void*)k_pcg_gate;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(32);
+    kp.kernelParams = args;
+    FL_CUDA(cudaGraphAddKernelNode(&gate, g.graph, nullptr, 0, &kp));
+  }
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = h;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
   cudaGraphNode_t node;
-  FL_CUDA(cudaGraphAddNode(&node, g.graph, nullptr, 0, &cp));
+  FL_CUDA(cudaGraphAddNode(&node, g.graph, gate ? &gate : nullptr, gate ? 1 : 0, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   FL_CUDA(cudaStreamBeginCaptureToGraph(gs->capture, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   const int st = enqueue_iteration(p, bits, sigma1, sigma2, x, work, h, gs->capture);
@@ -517,31 +574,40 @@ int fl_ipm_newton_step(fl_plan_t p, const uint32_t* bits, const fl_state* st, co
   int nb = 0;
   double rho = 0.0, flag = 0.0;
   FL_TRY(newton_setup(n, st, g, lam, mu, sigma1, sigma2, x, work, work + 2 * n, sc->partials, &nb, s));
-  FL_TRY(pcg_start_fetch(sc, nb, true, work + 6 * n, &rho, &flag, s));
-  if (flag != 0.0) return fail(FL_E_INTERIOR, "slacks and multipliers must be strictly positive and finite");
-  FL_TRY(check_rho(rho, 0));
   const int64_t limit = pcg_limit(n, max_iters);
   double* slots = work + 6 * n;
   PcgCtl* ctl = reinterpret_cast<PcgCtl*>(slots + 8);
   PcgCtl* hc = reinterpret_cast<PcgCtl*>(sc->host);
+  double* dev = sc->result + 32;
+  if (pcg_mode() == 3) {
+    // no sync at all: the start check runs in the graph's gate kernel
+    const int kinds[3] = {RED_SUM, RED_SUM, RED_MAX};
+    FL_TRY(finish_reduce(sc->partials, nb, 3, kinds, sc->result, s));
+    cudaGraphExec_t exec;
+    FL_TRY(pcg_graph(p, bits, sigma1, sigma2, x, work, &exec, true));
+    *hc = PcgCtl{0.0, 0.0, 0.0, (long long)limit, 0, 0, 0, abs_tol, rel_tol};
+    FL_CUDA(cudaMemcpyAsync(ctl, hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
+    FL_CUDA(cudaGraphLaunch(exec, s));
+    FL_TRY(ipm_step_device(n, st, sigma1, sigma2, mu, tau, x, x + n, &ctl->status, dev, s));
+    k_step_pack<<<1, 32, 0, s>>>(ctl, -1.0, dev);
+    FL_LAUNCH_CHECK();
+    FL_CUDA(cudaMemcpyAsync(host_out, dev, 13 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    return FL_OK;
+  }
+  FL_TRY(pcg_start_fetch(sc, nb, true, work + 6 * n, &rho, &flag, s));
+  if (flag != 0.0) return fail(FL_E_INTERIOR, "slacks and multipliers must be strictly positive and finite");
+  FL_TRY(check_rho(rho, 0));
   const double norm0 = std::sqrt(rho);
   const double thr = abs_tol + rel_tol * norm0;
   if (norm0 <= thr || limit <= 0) {
     *hc = PcgCtl{thr, norm0, 0.0, (long long)limit, 0, norm0 <= thr ? 1 : 2, 1};
     FL_CUDA(cudaMemcpyAsync(ctl, hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
-  } else if (pcg_mode() == 3) {
-    cudaGraphExec_t exec;
-    FL_TRY(pcg_graph(p, bits, sigma1, sigma2, x, work, &exec));
-    *hc = PcgCtl{thr, norm0, 0.0, (long long)limit, 0, 0, 0};
-    FL_CUDA(cudaMemcpyAsync(ctl, hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
-    FL_CUDA(cudaGraphLaunch(exec, s));
   } else {
     fl_pcg_result r{};
     FL_TRY(pcg_v2_loop(p, bits, sigma1, sigma2, x, work, rho, abs_tol, rel_tol, limit, &r, nullptr, 0, s));
     *hc = PcgCtl{thr, r.residual_norm, 0.0, (long long)limit, (long long)r.iterations, r.converged ? 1 : 2, 1};
     FL_CUDA(cudaMemcpyAsync(ctl, hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
   }
-  double* dev = sc->result + 32;
   FL_TRY(ipm_step_device(n, st, sigma1, sigma2, mu, tau, x, x + n, &ctl->status, dev, s));
   k_step_pack<<<1, 32, 0, s>>>(ctl, norm0, dev);
   FL_LAUNCH_CHECK();

@@ -27,7 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _dev, _lib
-from .errors import NumericalBreakdownError, StalledError
+from .errors import InteriorViolationError, NumericalBreakdownError, StalledError
 from .masking import Mask, embed_device
 from .newton_system import (
     BarrierDiagonals,
@@ -511,7 +511,11 @@ def _step_verdict(ws: Workspace):
     status, k = int(v[8]), int(v[9])
     if status == 3:
         raise NumericalBreakdownError(f"nonpositive curvature p'Kp = {v[11]:f} at iteration {k}")
+    if status == 5:
+        raise InteriorViolationError("slacks and multipliers must be strictly positive and finite")
     if status == 4:
+        if k == 0:
+            raise NumericalBreakdownError(f"preconditioner produced r'P^{{-1}}r = {v[11]:f}")
         raise NumericalBreakdownError(f"r'P^{{-1}}r = {v[11]:f} at iteration {k}")
     res = PcgResult(ws.x, k, status == 1, float(v[10]), None)
     if not res.converged:

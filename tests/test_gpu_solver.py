@@ -431,3 +431,46 @@ def test_one_sync_step_cap_skips_update():
     assert [getattr(ws.state, f).cpu().numpy().tobytes() for f in ipm.FIELDS] == before
     with pytest.raises(fl.NumericalBreakdownError, match="PCG stalled"):
         ipm._step_verdict(ws)
+
+
+def test_one_sync_step_gate_verdicts():
+    """The gated graph's start check (k_pcg_gate): a non-interior state gives
+    status 5 (InteriorViolationError, state untouched); a start residual
+    already below the threshold gives status 1 after 0 iterations and the
+    update runs, as on the host path."""
+    import ctypes
+
+    import torch
+
+    from paper_2502_04217_b200 import _dev, _lib
+
+    g = load_golden("solve_c1_4096")
+    dims = tuple(int(d) for d in g["dims"])
+    mask = fl.Mask(g["missing"], fl.GridShape(dims))
+    lam = float(g["lam"])
+    n = mask.shape.n
+    ws = ipm.Workspace(n)
+    prob = ipm.Problem(g["b"], mask, scratch=ws.work)
+
+    def step(abs_tol):
+        _lib.call("fl_ipm_newton_step", prob.plan.handle, _dev.ptr(prob.dmask.bits), ctypes.byref(ws.fs),
+                  _dev.ptr(ws.g), lam, lam / 2, 0.995, _dev.ptr(ws.sig1), _dev.ptr(ws.sig2), _dev.ptr(ws.x),
+                  _dev.ptr(ws.work), abs_tol, 0.0, 100, ws.verdict.data_ptr(), _dev.stream())
+        torch.cuda.synchronize()
+        return ws.verdict.tolist()
+
+    _lib.call("fl_ipm_init", n, ctypes.byref(ws.fs), lam, _dev.stream())
+    prob.residual_adjoint(ws.state.beta, ws.g)
+    ws.state.s1[3] = -1.0
+    before = [getattr(ws.state, f).cpu().numpy().tobytes() for f in ipm.FIELDS]
+    v = step(1e-12)
+    assert v[8] == 5 and v[6] == 1.0
+    assert [getattr(ws.state, f).cpu().numpy().tobytes() for f in ipm.FIELDS] == before
+    with pytest.raises(fl.InteriorViolationError):
+        ipm._step_verdict(ws)
+    _lib.call("fl_ipm_init", n, ctypes.byref(ws.fs), lam, _dev.stream())
+    v = step(1e300)
+    assert v[8] == 1 and v[9] == 0 and v[6] == 0.0 and v[10] == v[12]
+    res, ap, ad = ipm._step_verdict(ws)
+    assert res.iterations == 0 and res.converged and ap > 0
+    assert v[7] == 0.0
