@@ -116,3 +116,33 @@ def test_report_schema_keys():
     assert list(rec.to_dict()) == ["record", "iteration", "mu", "primal_inf", "dual_inf",
                                    "complementarity", "kkt_max", "krylov_iters", "alpha_primal",
                                    "alpha_dual", "pcg_residual", "centrality_ok", "wall_time"]
+
+
+def _verdict(status, k=3, norm=1e-9, bad=0.0, ap=0.5, ad=0.25, skip=0.0, interior=0.0):
+    import torch
+
+    v = torch.zeros(16, dtype=torch.float64)
+    v[4], v[5], v[6], v[7] = ap, ad, skip, interior
+    v[8], v[9], v[10], v[11], v[12] = status, k, norm, bad, 1.0
+    return type("WS", (), {"verdict": v, "x": None})()
+
+
+def test_step_verdict_maps_device_statuses_to_reference_errors():
+    """Host side of the one-sync IPM step (ipm._step_verdict): the device
+    verdict raises what the synchronous path raises, in the same order."""
+    res, ap, ad = ipm._step_verdict(_verdict(1))
+    assert (res.iterations, res.converged, ap, ad) == (3, True, 0.5, 0.25)
+    with pytest.raises(fl.InteriorViolationError):
+        ipm._step_verdict(_verdict(5, skip=1.0))
+    with pytest.raises(fl.NumericalBreakdownError, match="curvature"):
+        ipm._step_verdict(_verdict(3, bad=-1.0, skip=1.0))
+    with pytest.raises(fl.NumericalBreakdownError, match="preconditioner produced"):
+        ipm._step_verdict(_verdict(4, k=0, bad=float("nan"), skip=1.0))
+    with pytest.raises(fl.NumericalBreakdownError, match="at iteration 7"):
+        ipm._step_verdict(_verdict(4, k=7, bad=-2.0, skip=1.0))
+    with pytest.raises(fl.NumericalBreakdownError, match="PCG stalled"):
+        ipm._step_verdict(_verdict(2, skip=1.0))
+    with pytest.raises(fl.StalledError, match="collapsed"):
+        ipm._step_verdict(_verdict(1, ap=1e-13, skip=1.0))
+    with pytest.raises(fl.StalledError, match="interior"):
+        ipm._step_verdict(_verdict(1, interior=1.0))
