@@ -290,7 +290,7 @@ def weak_dims(world: int, side: int = 512):
 
 
 def run_sharded(args, comm, barrier, max_ms):
-    """Slab-sharded KKT matvec (+ solve) over comm.world ranks (real or emulated)."""
+    """Slab-sharded KKT matvec over comm.world ranks (real or emulated), device-timed and e2e."""
     import torch
 
     from paper_2502_04217_b200 import _dev, _lib
