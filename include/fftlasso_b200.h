@@ -154,6 +154,15 @@ FL_API int fl_mask_build(int64_t n, const uint8_t* flags, uint32_t* miss_bits, i
  * straight into bits + observed offsets, no host flags.  Synchronises. */
 FL_API int fl_mask_bragg(int ndim, const int64_t* dims, int64_t spacing, double radius, uint32_t* miss_bits,
                          int64_t* offsets, int64_t* n_observed, fl_stream_t stream);
+/* On-device observation noise for the C4/C5 recipes (no
+ * reference counterpart: the reference draws noise on the host,
+ * synthetic.py:45-63).  In place on a local box of a grid:
+ * x[k] = missing(k) ? 0 : x[k] + sigma * N(seed, g(k)), where k indexes the
+ * box ext[0] x ext[1] x ext[2] (row-major; miss_bits indexed by k) and
+ * g(k) = sum_a (l_a + off[a]) * stride[a] is the voxel's GLOBAL flat index,
+ * so the full grid, X-slabs and Y-slabs get bitwise the same draws. */
+FL_API int fl_noisy_embed(const int64_t* ext, const int64_t* off, const int64_t* stride, uint64_t seed,
+                          double sigma, const uint32_t* miss_bits, double* x, fl_stream_t stream);
 /* embed (masking.py:90-99): full = 0; full[observed] = obs. */
 FL_API int fl_embed(int64_t n, const uint32_t* miss_bits, const int64_t* obs_offsets,
              const double* obs, double* full, fl_stream_t stream);

@@ -63,6 +63,8 @@ SIGNATURES = {
     "fl_slab_pack_y": (_I, [_I64, _I64, _I64, _I, _P, _P, _P]),
     "fl_slab_unpack_y": (_I, [_I64, _I64, _I64, _I, _P, _P, _P]),
     "fl_mask_build": (_I, [_I64, _P, _P, _P, ctypes.POINTER(_I64), _P]),
+    "fl_noisy_embed": (_I, [ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.c_uint64,
+                            _D, _P, _P, _P]),
     "fl_embed": (_I, [_I64, _P, _P, _P, _P, _P]),
     "fl_gather_observed": (_I, [_I64, _P, _P, _P, _P, _P]),
     "fl_gram": (_I, [_P, _P, _P, _P, _P]),

@@ -36,13 +36,12 @@ Entry lookup(int m, bool strided, int kind, bool epi) {
   }
 }
 
+// Called once per (device, kernel): the shared-memory opt-in is a per-device
+// function attribute.
 int grid_of(Entry& e, int* out) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    FL_CUDA(cudaGetDevice(&dev));
-    FL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int dev = 0, sms = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  FL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   cudaFuncAttributes fa;
   FL_CUDA(cudaFuncGetAttributes(&fa, e.fn));
   FL_CUDA(cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -65,8 +64,9 @@ bool fast_supported(int m) { return m >= 16 && m <= 8192 && (m & (m - 1)) == 0; 
 int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int* nblocks,
                 cudaStream_t s) {
   // persistent grid size per kernel variant (resident CTAs x SMs)
+  // keyed by (device, kernel): attributes and SM counts are per device
   static std::mutex mu;
-  static std::unordered_map<const void*, int> grids;
+  static std::unordered_map<const void*, int> grids[kMaxDevices];
   // strided m = 1024 synthesis / analysis: the radix-2 split into two mirrored
   // 512-point halves (fl_split.cuh) wins on the large-stride axis (1024^3
   // axis 0: synthesis 7.44 -> 6.36 ms, analysis 7.43 -> 6.18 ms) and loses on
@@ -80,13 +80,15 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
                      (split_mode == 2 || (split_mode == 1 && A.inner >= 16384));
   Entry e = split ? fpk::make_split_1024(kind) : lookup(m, strided, kind, epi);
   if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");
-  int grid_cap = 0;
+  int grid_cap = 0, dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(FL_E_VALUE, "device index out of range");
   {
     std::lock_guard<std::mutex> lock(mu);
-    auto it = grids.find((const void*)e.fn);
-    if (it == grids.end()) {
+    auto it = grids[dev].find((const void*)e.fn);
+    if (it == grids[dev].end()) {
       FL_TRY(grid_of(e, &grid_cap));
-      grids[(const void*)e.fn] = grid_cap;
+      grids[dev][(const void*)e.fn] = grid_cap;
     } else {
       grid_cap = it->second;
     }

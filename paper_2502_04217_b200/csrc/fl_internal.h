@@ -32,6 +32,8 @@ struct fl_plan {
 
 namespace fl {
 
+constexpr int kMaxDevices = 16;  // per-device caches (scratch, kernel attributes)
+
 enum PassKind : int { K_SYNTH = 0, K_ANALYZE = 1, K_GRAM = 2, K_RESID = 3, K_COPY = 4 };
 
 struct KktEpi {

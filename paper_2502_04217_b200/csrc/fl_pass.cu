@@ -23,6 +23,8 @@
 #include <cstdlib>
 #include <string>
 
+#include <mutex>
+
 #include "fl_common.cuh"
 #include "fl_internal.h"
 #include "fl_passargs.cuh"
@@ -247,7 +249,8 @@ int run_pass(const fl_plan* p, int axis, int kind, const double* in, double* out
 int run_pass_n(const fl_plan* p, int axis, int kind, const double* in, double* out,
                const uint32_t* bits, const double* bhat, const KktEpi* epi, int* nblocks,
                double* nrm_partials, cudaStream_t s) {
-  static bool attrs_set[2][4][2] = {};
+  static std::mutex attrs_mu;
+  static bool attrs_set[kMaxDevices][2][4][2] = {};  // per-device smem opt-in
   const bool strided = axis < p->ndim - 1;
   if (!p->planned[axis]) return fail(FL_E_VALUE, "axis " + std::to_string(axis) + " is a batch extent of this plan");
   if ((kind == K_GRAM || kind == K_RESID) && strided)
@@ -294,10 +297,16 @@ int run_pass_n(const fl_plan* p, int axis, int kind, const double* in, double* o
   A.F = F;
   const bool has_epi = epi != nullptr;
   KernelFn k = strided ? pick_kernel<true>(kind, has_epi) : pick_kernel<false>(kind, has_epi);
-  bool& done = attrs_set[strided][kind][has_epi];
-  if (!done) {
-    FL_TRY(set_smem_attr(k));
-    done = true;
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(FL_E_VALUE, "device index out of range");
+  {
+    std::lock_guard<std::mutex> lock(attrs_mu);
+    bool& done = attrs_set[dev][strided][kind][has_epi];
+    if (!done) {
+      FL_TRY(set_smem_attr(k));
+      done = true;
+    }
   }
   const int64_t tiles = (A.G + F - 1) / F;
   const int grid = (int)std::min<int64_t>(tiles, kMaxGrid);

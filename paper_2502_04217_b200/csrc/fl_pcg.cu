@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "fl_common.cuh"
@@ -254,19 +255,34 @@ __global__ void k_step_pack(const PcgCtl* __restrict__ c, double norm0, double* 
   if (norm0 >= 0.0) dev[12] = norm0;  // < 0: written by the gate
 }
 
+// A captured graph bakes in every pointer it touches: the operands AND the
+// calling thread's reduction scratch (partials, result), so all of them are
+// the key.  Bounded LRU per plan (kPcgGraphCap entries); an evicted exec that
+// is still in flight is freed by the driver when it completes.
 struct PcgGraph {
   const uint32_t* bits;
   const double *sig1, *sig2;
   double *x, *work;
+  const double *partials, *result;
   bool gated;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
 
+constexpr size_t kPcgGraphCap = 4;
+
 struct PcgGraphs {
-  std::vector<PcgGraph> v;
+  std::vector<PcgGraph> v;  // least recently used first
   cudaStream_t capture = nullptr;
+  std::mutex mu;
 };
+
+void destroy_graph(PcgGraph& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (g.graph) cudaGraphDestroy(g.graph);
+  g.exec = nullptr;
+  g.graph = nullptr;
+}
 
 // Enqueue one v2 iteration with device-side scalars (captured into the body).
 int enqueue_iteration(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, double* x,
@@ -296,19 +312,33 @@ int enqueue_iteration(fl_plan_t p, const uint32_t* bits, const double* sigma1, c
 
 int pcg_graph(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, double* x,
               double* work, cudaGraphExec_t* out, bool gated = false) {
+  Scratch* sc0;
+  FL_TRY(scratch(&sc0));
   auto* gs = static_cast<PcgGraphs*>(p->pcg_graphs);
   if (!gs) {
-    gs = new PcgGraphs();
-    p->pcg_graphs = gs;
+    static std::mutex create_mu;
+    std::lock_guard<std::mutex> lock(create_mu);
+    if (!p->pcg_graphs) p->pcg_graphs = new PcgGraphs();
+    gs = static_cast<PcgGraphs*>(p->pcg_graphs);
   }
-  for (const PcgGraph& g : gs->v)
+  std::lock_guard<std::mutex> lock(gs->mu);
+  for (size_t i = 0; i < gs->v.size(); ++i) {
+    const PcgGraph& g = gs->v[i];
     if (g.bits == bits && g.sig1 == sigma1 && g.sig2 == sigma2 && g.x == x && g.work == work &&
-        g.gated == gated) {
-      *out = g.exec;
+        g.partials == sc0->partials && g.result == sc0->result && g.gated == gated) {
+      PcgGraph hit = g;
+      gs->v.erase(gs->v.begin() + (ptrdiff_t)i);
+      gs->v.push_back(hit);
+      *out = hit.exec;
       return FL_OK;
     }
+  }
   if (!gs->capture) FL_CUDA(cudaStreamCreateWithFlags(&gs->capture, cudaStreamNonBlocking));
-  PcgGraph g{bits, sigma1, sigma2, x, work, gated};
+  if (gs->v.size() >= kPcgGraphCap) {
+    destroy_graph(gs->v.front());
+    gs->v.erase(gs->v.begin());
+  }
+  PcgGraph g{bits, sigma1, sigma2, x, work, sc0->partials, sc0->result, gated};
   FL_CUDA(cudaGraphCreate(&g.graph, 0));
   cudaGraphConditionalHandle h;
   // gated: the loop starts closed and k_pcg_gate opens it
@@ -496,10 +526,7 @@ namespace fl {
 void pcg_graphs_release(fl_plan* p) {
   auto* gs = static_cast<PcgGraphs*>(p->pcg_graphs);
   if (!gs) return;
-  for (PcgGraph& g : gs->v) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    if (g.graph) cudaGraphDestroy(g.graph);
-  }
+  for (PcgGraph& g : gs->v) destroy_graph(g);
   if (gs->capture) cudaStreamDestroy(gs->capture);
   delete gs;
   p->pcg_graphs = nullptr;

@@ -23,7 +23,7 @@ int fail(int code, const std::string& msg) {
 
 // ---- reduction scratch, one per (host thread, device) ----
 struct ScratchSet {
-  Scratch s[16];
+  Scratch s[kMaxDevices];
   ~ScratchSet() {
     // process teardown: the CUDA context may already be gone, ignore errors
     for (auto& x : s) {
@@ -38,7 +38,7 @@ static thread_local ScratchSet g_scratch;
 int scratch(Scratch** out) {
   int dev = 0;
   FL_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 16) return fail(FL_E_VALUE, "device index out of range");
+  if (dev < 0 || dev >= kMaxDevices) return fail(FL_E_VALUE, "device index out of range");
   Scratch& s = g_scratch.s[dev];
   if (!s.partials) {
     if (cudaMalloc(&s.partials, sizeof(double) * kPartialSlots) != cudaSuccess ||

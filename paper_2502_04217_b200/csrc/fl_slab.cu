@@ -8,6 +8,9 @@
 // moves); Y-side kernels transpose (i0, i2) through 32x33 shared tiles.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
 
 #include "fl_common.cuh"
 #include "fl_internal.h"
@@ -87,17 +90,30 @@ __global__ void k_y_blocks(int64_t a, int64_t b, int64_t d2, int P, const double
 // NVSwitch for remote ranks, the local buffer for this rank).  The 32x33
 // shared tile turns the layout change into 256-byte coalesced row stores on
 // both sides.
+//
+// Ordering: the stores to peer slabs must be visible on the owning GPU before
+// it reads them.  Each CTA ends with a barrier and one system-scope fence
+// (cumulative over the CTA's stores, which the barrier ordered before it);
+// the caller then puts a stream-ordered cross-rank barrier (a one-element
+// NCCL all-reduce) between this kernel and the first read on the peer.
+//
+// The destination table (one slab pointer per rank) lives in device memory
+// (uploaded once per distinct table, see peer_table) and is read with a
+// uniform or per-thread global load -- no by-value pointer array indexed
+// dynamically (that forces a local-memory copy of the parameter block).
 constexpr int kMaxPeers = 16;
-struct Peers {
-  double* p[kMaxPeers];
-};
+
+__device__ __forceinline__ void publish_system() {
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
 
 // X-slab (a, d1, d2) of rank `me` -> Y-slabs (b, d2, d0) of every rank:
 //   Y[j / b][((j % b) d2 + i2) d0 + me a + i0] = x[(i0 d1 + j) d2 + i2]
 // One CTA per (j, 32x32 tile of (i0, i2)).
 // (ac planes starting at plane i0off of the slab: the chunked, overlapped form)
 __global__ void k_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int P, int me, const double* __restrict__ x,
-                               Peers dst, int64_t ac, int64_t i0off) {
+                               double* const* __restrict__ dst, int64_t ac, int64_t i0off) {
   __shared__ double tile[32][33];
   const int64_t b = d1 / P, d0 = a * P;
   const int64_t t0 = (ac + 31) / 32, t2 = (d2 + 31) / 32;
@@ -113,19 +129,20 @@ __global__ void k_x_to_y_peers(int64_t a, int64_t d1, int64_t d2, int P, int me,
     if (i0 < ac && i2 < d2) tile[k][tx] = x[(i0 * d1 + j) * d2 + i2];
   }
   __syncthreads();
-  double* y = dst.p[j / b];
+  double* y = dst[j / b];
   const int64_t j1 = j % b;
   for (int k = ty; k < 32; k += 8) {  // write: i0 fastest
     const int64_t i2 = base2 + k, i0 = base0 + tx;
     if (i0 < ac && i2 < d2) y[(j1 * d2 + i2) * d0 + me * a + i0off + i0] = tile[tx][k];
   }
+  publish_system();
 }
 
 // Y-slab (b, d2, d0) of rank `me` -> X-slabs (a, d1, d2) of every rank:
 //   X[i / a][((i % a) d1 + me b + j1) d2 + i2] = y[(j1 d2 + i2) d0 + i]
 // One CTA per (j1, 32x32 tile of (i, i2)).
 __global__ void k_y_to_x_peers(int64_t a, int64_t b, int64_t d2, int P, int me, const double* __restrict__ y,
-                               Peers dst) {
+                               double* const* __restrict__ dst) {
   __shared__ double tile[32][33];
   const int64_t d0 = a * P, d1 = b * P;
   const int64_t ti_n = (d0 + 31) / 32, t2 = (d2 + 31) / 32;
@@ -143,16 +160,34 @@ __global__ void k_y_to_x_peers(int64_t a, int64_t b, int64_t d2, int P, int me, 
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {  // write: i2 fastest
     const int64_t i = base + k, i2 = base2 + tx;
-    if (i < d0 && i2 < d2) dst.p[i / a][((i % a) * d1 + me * b + j1) * d2 + i2] = tile[k][tx];
+    if (i < d0 && i2 < d2) dst[i / a][((i % a) * d1 + me * b + j1) * d2 + i2] = tile[k][tx];
   }
+  publish_system();
 }
 
-int peers_of(int P, double* const* ptrs, Peers* out) {
+// Device copy of a host pointer table, cached per (device, table contents):
+// a grid's exchange tables are fixed for its lifetime, so each is uploaded
+// once (a few distinct tables per process; never freed before exit).
+int peer_table(int P, double* const* ptrs, double* const** out) {
   if (P < 1 || P > kMaxPeers) return fail(FL_E_VALUE, "peer exchange supports 1..16 ranks");
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  std::vector<uintptr_t> key(1, (uintptr_t)dev);
   for (int r = 0; r < P; ++r) {
     if (!ptrs[r]) return fail(FL_E_VALUE, "null peer pointer");
-    out->p[r] = ptrs[r];
+    key.push_back((uintptr_t)ptrs[r]);
   }
+  static std::mutex mu;
+  static std::map<std::vector<uintptr_t>, double**> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    double** d = nullptr;
+    FL_CUDA(cudaMalloc(&d, sizeof(double*) * P));
+    FL_CUDA(cudaMemcpy(d, ptrs, sizeof(double*) * P, cudaMemcpyHostToDevice));
+    it = cache.emplace(key, d).first;
+  }
+  *out = it->second;
   return FL_OK;
 }
 
@@ -215,8 +250,8 @@ int fl_slab_x_to_y_peers_planes(int64_t a, int64_t d1, int64_t d2, int nranks, i
   if (!x_planes || !y_slabs) return fail(FL_E_VALUE, "null argument");
   if (nranks < 1 || d1 % nranks || rank < 0 || rank >= nranks) return fail(FL_E_SHAPE, "bad slab geometry");
   if (i0_begin < 0 || i0_count < 0 || i0_begin + i0_count > a) return fail(FL_E_SHAPE, "plane range outside the slab");
-  Peers pe;
-  FL_TRY(peers_of(nranks, y_slabs, &pe));
+  double* const* pe = nullptr;
+  FL_TRY(peer_table(nranks, y_slabs, &pe));
   const int64_t blocks = d1 * ((i0_count + 31) / 32) * ((d2 + 31) / 32);
   if (blocks > 0x7fffffffLL) return fail(FL_E_SHAPE, "slab too large");
   if (blocks == 0) return FL_OK;
@@ -235,8 +270,8 @@ int fl_slab_y_to_x_peers(int64_t a, int64_t b, int64_t d2, int nranks, int rank,
                          double* const* x_slabs, fl_stream_t stream) {
   if (!y_slab || !x_slabs) return fail(FL_E_VALUE, "null argument");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(FL_E_SHAPE, "bad slab geometry");
-  Peers pe;
-  FL_TRY(peers_of(nranks, x_slabs, &pe));
+  double* const* pe = nullptr;
+  FL_TRY(peer_table(nranks, x_slabs, &pe));
   const int64_t blocks = b * ((a * nranks + 31) / 32) * ((d2 + 31) / 32);
   if (blocks > 0x7fffffffLL) return fail(FL_E_SHAPE, "slab too large");
   if (blocks == 0) return FL_OK;

@@ -115,6 +115,38 @@ __global__ void k_embed(int64_t n, const uint32_t* __restrict__ bits, const int6
   }
 }
 
+// Counter-based observation noise for on-device inputs:
+// the draw of a voxel is a function of (seed, GLOBAL flat voxel index) only,
+// so a full grid, an X-slab and a Y-slab (any rank count) see bitwise the same
+// noise.  Local index k -> local coordinates (l0, l1, l2) in the box `ext`;
+// global index = sum_a (l_a + off_a) * stride_a.  Two splitmix64 words ->
+// Box-Muller (cosine branch), u1 in (0, 1].
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_noisy_embed(int64_t nl, int64_t e1, int64_t e2, int64_t o0, int64_t o1, int64_t o2, int64_t s0,
+                              int64_t s1, int64_t s2, uint64_t seed, double sigma,
+                              const uint32_t* __restrict__ bits, double* __restrict__ x) {
+  GRID_LOOP(k, nl) {
+    const bool miss = (bits[k >> 5] >> (k & 31)) & 1u;
+    if (miss) {
+      x[k] = 0.0;
+      continue;
+    }
+    const int64_t l2 = k % e2, t = k / e2;
+    const int64_t l1 = t % e1, l0 = t / e1;
+    const uint64_t g = (uint64_t)((l0 + o0) * s0 + (l1 + o1) * s1 + (l2 + o2) * s2);
+    const uint64_t h1 = mix64(seed ^ mix64(2 * g)), h2 = mix64(seed ^ mix64(2 * g + 1));
+    const double u1 = (double)((h1 >> 11) + 1) * 0x1.0p-53;
+    const double u2 = (double)(h2 >> 11) * 0x1.0p-53;
+    x[k] = __dadd_rn(x[k], __dmul_rn(sigma, __dmul_rn(sqrt(-2.0 * log(u1)), cospi(2.0 * u2))));
+  }
+}
+
 __global__ void k_gather(int64_t n, const uint32_t* __restrict__ bits, const int64_t* __restrict__ off,
                          const double* __restrict__ full, double* __restrict__ obs) {
   GRID_LOOP(v, n) {
@@ -949,6 +981,18 @@ int fl_mask_bragg(int ndim, const int64_t* dims, int64_t spacing, double radius,
   k_bragg_bits<<<grid_for(nw, T, 1 << 16), T, 0, s>>>(n, ndim, d1, d2, spacing, radius * radius, bits, offsets);
   FL_LAUNCH_CHECK();
   return mask_offsets(nw, offsets, n_observed, s);
+}
+
+int fl_noisy_embed(const int64_t* ext, const int64_t* off, const int64_t* stride, uint64_t seed, double sigma,
+                   const uint32_t* miss_bits, double* x, fl_stream_t stream) {
+  if (!ext || !off || !stride || !miss_bits || !x) return fail(FL_E_VALUE, "null argument");
+  if (ext[0] < 0 || ext[1] < 1 || ext[2] < 1) return fail(FL_E_SHAPE, "bad local box");
+  const int64_t nl = ext[0] * ext[1] * ext[2];
+  if (nl == 0) return FL_OK;
+  k_noisy_embed<<<grid_for(nl, T, 1 << 16), T, 0, (cudaStream_t)stream>>>(
+      nl, ext[1], ext[2], off[0], off[1], off[2], stride[0], stride[1], stride[2], seed, sigma, miss_bits, x);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
 }
 
 int fl_embed(int64_t n, const uint32_t* bits, const int64_t* off, const double* obs, double* full,

@@ -599,7 +599,10 @@ def solve(b, mask: Mask, config: IpmConfig = IpmConfig(),
             best_kkt = conv.max_residual
             ws.best_beta.copy_(st.beta)
         if observer is not None:
-            observer(st.to_numpy() if host else st, record)
+            # a fresh state per call, as the reference passes (ipm.py:382-393):
+            # the solver updates st in place
+            observer(st.to_numpy() if host else
+                     IpmState(mu=st.mu, **{f: getattr(st, f).clone() for f in FIELDS}), record)
     else:
         if conv.converged:
             status = "converged"

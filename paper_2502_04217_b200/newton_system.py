@@ -140,7 +140,9 @@ def _apply_kkt_streamed(d_beta, d_z, diag: BarrierDiagonals, mask: Mask):
     if hb.numel() != n or hz.numel() != n:
         raise UnsupportedShapeError(f"direction blocks must have {n} entries")
     dev = _dev.device()
-    h2d, d2h = _copy_streams.setdefault(dev.index, (torch.cuda.Stream(dev), torch.cuda.Stream(dev)))
+    if dev.index not in _copy_streams:
+        _copy_streams[dev.index] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    h2d, d2h = _copy_streams[dev.index]
     comp = torch.cuda.current_stream()
     g1, g2 = _vec(diag.sigma1, n), _vec(diag.sigma2, n)
     db, dz, top, bot = (_dev.empty(n) for _ in range(4))

@@ -481,10 +481,12 @@ class ShardedGrid:
         for op, y in zip(self.ops, ys):
             op.synth_y0(y, y)
 
-    def gram(self, betas, outs, bits_y, bhat_y=None, want_norm=False):
+    def gram(self, betas, outs, bits_y, bhat_y=None, want_norm=False, extra=None):
         """outs = A^T Z A beta (bhat_y None) or A^T Z (b_hat - A beta); X-slabs in/out.
 
-        Returns the all-reduced ||Z A beta||^2 when ``want_norm`` (gram only).
+        Returns the all-reduced ||Z A beta||^2 when ``want_norm`` (gram only);
+        with ``extra`` (one local partial per shard) the same all-reduce also
+        sums those and returns (norm, extra_sum).
         """
         if not self._overlapped_forward(betas, outs):
             for op, b, o in zip(self.ops, betas, outs):
@@ -497,6 +499,9 @@ class ShardedGrid:
         for op, x, o in zip(self.ops, src, outs):
             op.analyze_x(x, o)
         if want_norm:
+            if extra is not None:
+                red = self.comm.reduce([[v, e] for v, e in zip(norms, extra)], SUM)
+                return float(red[0]), float(red[1])
             return float(self.comm.reduce([[v] for v in norms], SUM)[0])
         return None
 
@@ -555,6 +560,76 @@ class ShardedProblem:
             bits.append(grid.ops[0].bits(grid.geo.y_slab(np.asarray(flags, dtype=np.uint8), r)))
             bh.append(grid.ops[0].vec(grid.geo.y_slab(np.asarray(b_hat_full, dtype=np.float64), r)))
         return cls(grid, bits, bh)
+
+
+def c4_problem_device(grid: ShardedGrid, noise_seed: int = 0, spacing: int = 16, radius: float = 5.3):
+    """The C4/C5 recipe built on the devices straight into slab layout
+    (no full-grid host array) -> (ShardedProblem, idx, val, lam).
+
+    Same input as ``workloads.c4_const_device`` on one GPU: the recipe's
+    spikes (``workloads.c4_spikes``) scattered into each X-slab, the sharded
+    synthesis to Y-slabs, then ``fl_noisy_embed`` in Y layout -- the noise is
+    a function of the global voxel index, so b_hat is the single-GPU one up
+    to the transforms' rounding (their axis order differs).  The Y-slab mask
+    is the Bragg mask of the local box (b, d2, d0) when b is a multiple of
+    ``spacing`` (the periodic distance of i1 = r b + j1 is then that of j1),
+    else the host formula (``bragg_y_flags``).
+    """
+    import torch
+
+    from . import workloads
+
+    geo = grid.geo
+    d0, d1, d2 = geo.dims
+    nl = geo.n_local
+    idx, val = workloads.c4_spikes(geo.n)
+    idx_t = torch.from_numpy(idx).to(_dev.device())
+    val_t = torch.from_numpy(val).to(_dev.device())
+    betas, bits = [], []
+    for r in grid.comm.ranks:
+        bx = _dev.empty(nl)
+        bx.zero_()
+        sel = (idx_t >= r * nl) & (idx_t < (r + 1) * nl)
+        bx[idx_t[sel] - r * nl] = val_t[sel]
+        betas.append(bx)
+        if geo.b % spacing == 0:
+            nw = (nl + 31) // 32
+            w = torch.empty(nw, dtype=torch.int32, device=_dev.device())
+            offs = torch.empty(nw, dtype=torch.int64, device=_dev.device())
+            dims = (ctypes.c_int64 * 3)(geo.b, d2, d0)
+            n_obs = ctypes.c_int64()
+            _lib.call("fl_mask_bragg", 3, dims, int(spacing), float(radius), _dev.ptr(w), _dev.ptr(offs),
+                      ctypes.byref(n_obs), _dev.stream())
+            del offs
+            bits.append(w)
+        else:
+            bits.append(grid.ops[0].bits(bragg_y_flags(geo, r, spacing, radius)))
+    ys = [_dev.empty(nl) for _ in grid.comm.ranks]
+    grid.synthesize_to_y(betas, ys)
+    del betas
+    for i, r in enumerate(grid.comm.ranks):
+        # Y-slab local box (b, d2, d0) = global (i1 = r b + j1, i2, i0)
+        workloads.noisy_embed_device(ys[i], bits[i], (geo.b, d2, d0), (r * geo.b, 0, 0), (d2, 1, d1 * d2),
+                                     noise_seed)
+    return ShardedProblem(grid, bits, ys), idx, val, 0.5
+
+
+def gather_support(betas, geo: SlabGeometry, comm: Comm, rel: float = 1e-6):
+    """Global indices of |beta| > rel * max|beta| over all slabs (diagnostics
+    classify_support threshold) -> sorted int64 array on every process."""
+    import torch
+
+    mx = float(comm.reduce([[float(b.abs().max())] for b in betas], MAX)[0])
+    thr = rel * mx
+    local = [torch.nonzero(b.abs() > thr).flatten().cpu().numpy() + r * geo.n_local
+             for b, r in zip(betas, comm.ranks)]
+    if isinstance(comm, DistComm):
+        import torch.distributed as dist
+
+        out = [None] * comm.world
+        dist.all_gather_object(out, local[0], group=comm.group)
+        local = out
+    return np.sort(np.concatenate(local)) if local else np.zeros(0, np.int64)
 
 
 def pack_bits(flags: np.ndarray) -> np.ndarray:
@@ -717,8 +792,13 @@ def _sharded_pcg(grid: ShardedGrid, prob: ShardedProblem, ws, cfg: PcgConfig):
     thr = cfg.abs_tol + cfg.rel_tol * norm
     if norm <= thr:
         return 0, norm
+    dq_parts = None  # local p.(K - G)p partials of the previous p-update
     for k in range(1, limit + 1):
-        curv_g = grid.gram([w.p[:nl] for w in ws], [w.gp for w in ws], prob.bits_y, want_norm=True)
+        if dq_parts is None:
+            curv_g = grid.gram([w.p[:nl] for w in ws], [w.gp for w in ws], prob.bits_y, want_norm=True)
+        else:  # one all-reduce for ||Z A p||^2 and the diagonal form
+            curv_g, dq = grid.gram([w.p[:nl] for w in ws], [w.gp for w in ws], prob.bits_y, want_norm=True,
+                                   extra=dq_parts)
         curv = curv_g + dq
         if not math.isfinite(curv) or curv <= 0:
             raise NumericalBreakdownError(f"nonpositive curvature p'Kp = {curv} at iteration {k}")
@@ -736,12 +816,11 @@ def _sharded_pcg(grid: ShardedGrid, prob: ShardedProblem, ws, cfg: PcgConfig):
         if norm <= thr:
             return k, norm
         beta = rho_next / rho
-        parts = []
+        dq_parts = []
         for w in ws:
             out = ctypes.c_double()
             _lib.check(L.fl_pcg_step_pupdate(nl, _dev.ptr(w.sig1), _dev.ptr(w.sig2), _dev.ptr(w.r), float(beta),
                                              _dev.ptr(w.p), ctypes.byref(out), s))
-            parts.append([out.value])
-        dq = float(comm.reduce(parts, SUM)[0])
+            dq_parts.append(out.value)
         rho = rho_next
     raise NumericalBreakdownError(f"PCG stalled at preconditioned residual {norm:.3e} after {limit} iterations")

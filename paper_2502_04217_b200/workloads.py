@@ -109,14 +109,42 @@ def c4_const(n_side: int) -> Instance:
     return Instance((n_side,) * 3, beta, flags, 0.05 * rng.standard_normal(n_obs), 0.5)
 
 
+C4_SEED = 1234
+C4_SIGMA = 0.05
+
+
+def c4_spikes(n: int):
+    """The C4/C5 recipe's sparse spectrum: global flat indices and values
+    (c4_const's own host RNG stream, only n/10^4 positions)."""
+    rng = np.random.default_rng(C4_SEED)
+    nnz = max(8, n // 10000)
+    idx = rng.choice(n, nnz, replace=False)
+    val = rng.uniform(1, 2, nnz) * rng.choice([-1., 1.], nnz)
+    return idx, val
+
+
+def noisy_embed_device(x, bits, ext, off, stride, noise_seed: int, sigma: float = C4_SIGMA):
+    """In place: x = Z (x + sigma * noise), noise drawn per GLOBAL voxel index
+    (``fl_noisy_embed``), so a full grid and any slab decomposition of it get
+    bitwise the same draws."""
+    import ctypes
+
+    from . import _dev, _lib
+
+    arr = lambda v: (ctypes.c_int64 * 3)(*[int(t) for t in v])  # noqa: E731
+    _lib.call("fl_noisy_embed", arr(ext), arr(off), arr(stride), int(noise_seed) & (2 ** 64 - 1), float(sigma),
+              _dev.ptr(bits), _dev.ptr(x), _dev.stream())
+
+
 def c4_const_device(n_side: int, noise_seed: int = 0):
     """C4/C5 recipe generated on the GPU -> (mask, b, beta_idx, beta_val, lam).
 
     The Bragg mask is built on the device (``masking.BraggMask``, bit-equal
-    to ``bragg_flags``); the spikes are c4_const's own (same host RNG stream,
-    only n/10^4 positions); the observation noise is drawn on the device with
-    torch's Philox generator, so ``b`` is NOT NumPy-identical to c4_const --
-    a C5-scale input without any n-sized host array.
+    to ``bragg_flags``); the spikes are c4_const's own (``c4_spikes``); the
+    observation noise is drawn on the device per global voxel index
+    (``fl_noisy_embed``), so ``b`` is NOT NumPy-identical to c4_const, but it
+    IS identical to the slab-sharded recipe (``sharded.c4_problem_device``)
+    -- a C5-scale input without any n-sized host array.
     """
     import torch
 
@@ -126,19 +154,16 @@ def c4_const_device(n_side: int, noise_seed: int = 0):
 
     shape = GridShape((n_side,) * 3)
     n = shape.n
-    rng = np.random.default_rng(1234)
-    nnz = max(8, n // 10000)
-    idx = rng.choice(n, nnz, replace=False)
-    val = rng.uniform(1, 2, nnz) * rng.choice([-1., 1.], nnz)
+    idx, val = c4_spikes(n)
     mask = BraggMask(shape)
     beta = torch.zeros(n, dtype=torch.float64, device=_dev.device())
     beta[torch.from_numpy(idx).to(beta.device)] = torch.from_numpy(val).to(beta.device)
     x = synthesize(beta, shape)
     del beta
+    d = n_side
+    noisy_embed_device(x, mask.on_device().bits, (d, d, d), (0, 0, 0), (d * d, d, 1), noise_seed)
     b = restrict(x, mask)
     del x
-    g = torch.Generator(device=b.device).manual_seed(noise_seed)
-    b += 0.05 * torch.randn(b.numel(), dtype=torch.float64, device=b.device, generator=g)
     return mask, b, idx, val, 0.5
 
 

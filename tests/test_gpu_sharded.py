@@ -167,3 +167,75 @@ def test_sharded_solve_8_ranks_c4_recipe_64():
     assert all(abs(x - y) <= 1 for x, y in zip(rep.krylov_counts, rep1.krylov_counts))
     assert abs(rep.final_objective - rep1.final_objective) <= 1e-9 * abs(rep1.final_objective)
     assert np.linalg.norm(beta - beta1) <= 1e-8 * np.linalg.norm(beta1)
+
+
+def test_noise_is_a_function_of_the_global_voxel():
+    """fl_noisy_embed: full grid vs X-slabs vs Y-slabs give bitwise the same
+    noisy, masked volume (the draws are keyed by the global voxel index)."""
+    import torch
+
+    from paper_2502_04217_b200 import workloads
+
+    dims = (32, 64, 48)
+    d0, d1, d2 = dims
+    P = 4
+    geo = sh.SlabGeometry(dims, P)
+    flags = np.random.default_rng(9).random(geo.n) < 0.2
+    x = np.random.default_rng(10).standard_normal(geo.n)
+    full = fl._dev.to_dev(x)
+    bits = torch.from_numpy(sh.pack_bits(flags)).cuda()
+    workloads.noisy_embed_device(full, bits, dims, (0, 0, 0), (d1 * d2, d2, 1), 77)
+    ref = full.cpu().numpy()
+    assert np.all(ref[flags] == 0.0)
+    noise = (ref - x)[~flags]
+    assert abs(noise.std() / 0.05 - 1) < 0.05 and abs(noise.mean()) < 0.01 * 0.05 * 10
+    for r in range(P):
+        xs = fl._dev.to_dev(geo.x_slab(x, r).copy())
+        bx = torch.from_numpy(sh.pack_bits(geo.x_slab(flags, r))).cuda()
+        workloads.noisy_embed_device(xs, bx, (geo.a, d1, d2), (r * geo.a, 0, 0), (d1 * d2, d2, 1), 77)
+        assert xs.cpu().numpy().tobytes() == geo.x_slab(ref, r).tobytes()
+        ys = fl._dev.to_dev(geo.y_slab(x, r))
+        by = torch.from_numpy(sh.pack_bits(geo.y_slab(flags.astype(np.uint8), r))).cuda()
+        workloads.noisy_embed_device(ys, by, (geo.b, d2, d0), (r * geo.b, 0, 0), (d2, 1, d1 * d2), 77)
+        assert ys.cpu().numpy().tobytes() == geo.y_slab(ref, r).tobytes()
+
+
+def test_sharded_solve_8_ranks_device_inputs_256():
+    """The C5 pipeline at 256^3 with P = 8 emulated ranks (LocalComm, peer
+    exchange): inputs generated on the device straight into slab layout
+    (sharded.c4_problem_device) against the single-GPU device recipe
+    (workloads.c4_const_device) -- same mask bits and b_hat, same solve."""
+    import torch
+
+    from paper_2502_04217_b200 import workloads
+
+    side = 256
+    mask, b, idx, _, lam = workloads.c4_const_device(side)
+    beta1, rep1 = fl.solve(b, mask, fl.IpmConfig(lam=lam))
+    dm = mask.on_device()
+    bhat = torch.zeros(side ** 3, dtype=torch.float64, device="cuda")
+    fl._lib.call("fl_embed", side ** 3, fl._dev.ptr(dm.bits), fl._dev.ptr(dm.offsets), fl._dev.ptr(b),
+                 fl._dev.ptr(bhat), fl._dev.stream())
+    bhat = bhat.cpu().numpy()
+    flags = mask.missing_bool
+    del b, dm
+    grid = sh.ShardedGrid((side,) * 3, sh.LocalComm(8), exchange="peer")
+    prob, idx2, _, lam2 = sh.c4_problem_device(grid, noise_seed=0)
+    assert lam2 == lam and np.array_equal(idx, idx2)
+    geo = grid.geo
+    for r in range(8):
+        want = sh.pack_bits(geo.y_slab(flags.astype(np.uint8), r))
+        assert prob.bits_y[r].cpu().numpy().tobytes() == want.tobytes()
+        got = prob.bhat_y[r].cpu().numpy()
+        exp = geo.y_slab(bhat, r)
+        assert np.max(np.abs(got - exp)) <= 1e-12 * np.abs(exp).max()
+    betas, rep = sh.sharded_solve(prob, lam, fl.IpmConfig(lam=lam))
+    assert rep.status == rep1.status == "converged"
+    assert abs(rep.iterations - rep1.iterations) <= 1
+    assert all(abs(x - y) <= 1 for x, y in zip(rep.krylov_counts, rep1.krylov_counts))
+    assert abs(rep.final_objective - rep1.final_objective) <= 1e-9 * abs(rep1.final_objective)
+    beta = geo.from_x([t.cpu().numpy() for t in betas])
+    b1 = beta1.cpu().numpy()
+    assert np.linalg.norm(beta - b1) <= 1e-8 * np.linalg.norm(b1)
+    found = sh.gather_support(betas, geo, grid.comm)
+    np.testing.assert_array_equal(found, np.sort(idx))
