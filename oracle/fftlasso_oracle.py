@@ -544,6 +544,58 @@ def support(beta, threshold=None):
             np.flatnonzero(np.abs(beta) <= threshold), float(threshold))
 
 
+def dense_gram(mask: OMask) -> np.ndarray:
+    """diagnostics.py:86-91 -- M_perp^T M_perp from the trig-formula matrix."""
+    a = dense_synthesis(mask.dims)[~mask.missing_bool, :]
+    return a.T @ a
+
+
+def dense_condensed(st, mask: OMask):
+    """diagnostics.py:94-108 -- dense (K, P) of the condensed system at an iterate."""
+    _, _, lam1, lam2, _, _ = diagonals(st.s1, st.s2, st.nu1, st.nu2)
+    g = dense_gram(mask)
+    k = np.block([[g + np.diag(lam1), np.diag(lam2)], [np.diag(lam2), np.diag(lam1)]])
+    p = np.block([[np.diag(1.0 + lam1), np.diag(lam2)], [np.diag(lam2), np.diag(lam1)]])
+    return k, p
+
+
+def dense_augmented(st, mask: OMask) -> np.ndarray:
+    """Reference tests/conftest.py:20-39 -- the 6n x 6n symmetrised Newton
+    matrix in the order (d_beta, d_z, d_s1, d_s2, d_y1, d_y2)."""
+    n = np.asarray(st.beta).size
+    g = dense_gram(mask)
+    i, z = np.eye(n), np.zeros((n, n))
+    sg1, sg2 = np.diag(st.nu1 / st.s1), np.diag(st.nu2 / st.s2)
+    return np.block([[g, z, z, z, -i, i], [z, z, z, z, -i, -i], [z, z, sg1, z, -i, z],
+                     [z, z, z, sg2, z, -i], [-i, -i, -i, z, z, z], [i, -i, z, -i, z, z]])
+
+
+def preconditioned_spectrum(st, mask: OMask, cluster_tol: float = 0.05, support_threshold=None) -> dict:
+    """diagnostics.py:183-224 -- dense eigen-probe of P^-1 K (as K v = l P v)."""
+    import scipy.linalg
+
+    n = np.asarray(st.beta).size
+    if n > 1024:
+        raise ValueError(f"spectrum probe guard: n {n} > 1024")
+    k, p = dense_condensed(st, mask)
+    eigs = scipy.linalg.eigh(k, p, eigvals_only=True)
+    eigs_k = scipy.linalg.eigvalsh(k)
+    pos, neg, _, _ = support(st.beta, support_threshold)
+    active = np.sort(np.concatenate([pos, neg]))
+    if active.size:
+        q_eigs = scipy.linalg.eigvalsh(dense_gram(mask)[np.ix_(active, active)])
+        kappa_pred = max(1.0, float(q_eigs[-1])) / min(1.0, float(q_eigs[0]))
+    else:
+        kappa_pred = 1.0
+    comp_floor = min(float(np.min(st.s1 + st.nu1)), float(np.min(st.s2 + st.nu2)))
+    return dict(eigenvalues=eigs, unit_cluster_size=int(np.sum(np.abs(eigs - 1.0) <= cluster_tol)),
+                predicted_cluster_size=2 * n - int(active.size),
+                kappa_observed=float(eigs[-1] / eigs[0]), kappa_predicted=kappa_pred,
+                kappa_unpreconditioned=float(eigs_k[-1] / eigs_k[0]), n_active=int(active.size),
+                strict_complementarity=comp_floor,
+                duality_measure=(float(np.dot(st.nu1, st.s1)) + float(np.dot(st.nu2, st.s2))) / (2 * n))
+
+
 def ista(b, mask: OMask, lam: float, tol: float = 1e-10, max_iters: int = 10**6):
     """diagnostics.py:331-360 without the n <= 4096 guard -> (beta, iterations).
 

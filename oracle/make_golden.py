@@ -294,6 +294,40 @@ def ista():
     save("ista", **arrays)
 
 
+def spectrum():
+    """Reference dense probes (diagnostics.py:94-224) on observer snapshots of a
+    reference solve -> tests/golden/spectrum.npz (pins the oracle's restatement)."""
+    from fftlasso import diagnostics as ref_diag
+
+    rng = np.random.default_rng(7005)
+    n = 24
+    miss = np.sort(rng.choice(n, 3, replace=False))
+    g = ref.GridShape((n,))
+    mask = ref.Mask(miss, g)
+    bt = np.zeros(n)
+    bt[[2, 7]] = [1.5, -1.1]
+    b = ref.observe(bt, mask) + 0.02 * rng.standard_normal(mask.n_observed)
+    states = []
+    fields = ("beta", "z", "s1", "s2", "y1", "y2", "nu1", "nu2")
+    ref.solve(b, mask, ref_ipm.IpmConfig(lam=0.35, tol=1e-8),
+              observer=lambda s, r: states.append(ref_ipm.IpmState(mu=s.mu, **{f: getattr(s, f).copy() for f in fields})))
+    arrays = dict(missing=miss)
+    om = orc.make_mask((n,), missing=miss)
+    for tag, st in (("first", states[0]), ("last", states[-1])):
+        rep = ref_diag.preconditioned_spectrum(st, mask)
+        k, p = ref_diag.dense_condensed_matrices(st, mask)
+        for f in fields:
+            arrays[f"{tag}__{f}"] = getattr(st, f)
+        arrays[f"{tag}__eigs"] = rep.eigenvalues
+        arrays[f"{tag}__K"] = k
+        arrays[f"{tag}__P"] = p
+        arrays[f"{tag}__scalars"] = np.array([rep.unit_cluster_size, rep.predicted_cluster_size, rep.kappa_observed,
+                                              rep.kappa_predicted, rep.kappa_unpreconditioned, rep.n_active,
+                                              rep.strict_complementarity, rep.duality_measure])
+        note("spectrum", rep.eigenvalues, orc.preconditioned_spectrum(st, om)["eigenvalues"])
+    save("spectrum", **arrays)
+
+
 def _strip_wall(rows):
     return [{k: v for k, v in r.items() if k != "wall_time"} for r in rows]
 
@@ -344,7 +378,7 @@ if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
     for name, fn in (("transforms", transforms), ("masking", masking), ("newton", newton),
-                     ("solves", solves), ("cli", cli), ("ista", ista)):
+                     ("solves", solves), ("cli", cli), ("ista", ista), ("spectrum", spectrum)):
         if not only or name in only:
             print(name)
             fn()

@@ -12,9 +12,16 @@
   ISTA can check IPM objectives at sizes where no CPU or dense oracle runs
   (SURVEY §8f item 2).
 
-The dense-matrix probes of the reference (``densify``, spectrum and scaling
-probes) are test tooling built on O(n^2) dense matrices, outside the hot
-path; IPM state snapshots for such probes come from ``solve``'s observer.
+* ``scaling_trajectory_check`` / ``ScalingReport`` -- the barrier-scaling
+  probe over the tail of an IPM trajectory (diagnostics.py:234-322), with the
+  barrier diagonals and the per-class ratio ranges computed on the GPU; the
+  trajectory is the list of states ``solve``'s observer receives (a fresh
+  snapshot per iteration, as the reference passes).
+
+The dense-matrix probes of the reference (``densify``, the dense spectrum
+probe) are O(n^2)-O(n^3) test tooling outside the hot path; the GPU test
+suite runs them from the oracle (``oracle/fftlasso_oracle.py``) on the
+observer's snapshots of GPU solves (reference acceptance criteria 5-6).
 """
 
 from __future__ import annotations
@@ -35,6 +42,8 @@ __all__ = [
     "classify_support",
     "soft_threshold",
     "ista_solve",
+    "ScalingReport",
+    "scaling_trajectory_check",
 ]
 
 ISTA_DIM_GUARD = 4096
@@ -115,3 +124,72 @@ def ista_solve(b, mask: Mask, lam: float, tol: float = 1e-10,
         if step.value <= tol:
             return _dev.out(beta, host), k
     raise IterationLimitError(f"ISTA did not reach tol={tol:.1e} within {max_iters} iterations")
+
+
+@dataclass
+class ScalingReport:
+    """Observed barrier scaling ratios over the tail of a trajectory (diagnostics.py:234-268)."""
+
+    band: tuple
+    iterations_checked: int
+    lambda1_times_mu: tuple
+    sigma1_over_mu_pos: tuple
+    sigma2_times_mu_pos: tuple
+    sigma1_times_mu_neg: tuple
+    sigma2_over_mu_neg: tuple
+    sigma1_times_mu_zero: tuple
+    sigma2_times_mu_zero: tuple
+    sigma_product_active: tuple
+    in_band: bool
+
+    def to_dict(self) -> dict:
+        out = {"record": "scaling", "band": list(self.band), "iterations_checked": self.iterations_checked}
+        for k in ("lambda1_times_mu", "sigma1_over_mu_pos", "sigma2_times_mu_pos", "sigma1_times_mu_neg",
+                  "sigma2_over_mu_neg", "sigma1_times_mu_zero", "sigma2_times_mu_zero", "sigma_product_active"):
+            out[k] = list(getattr(self, k))
+        out["in_band"] = self.in_band
+        return out
+
+
+def scaling_trajectory_check(states, support: SupportClassification | None = None,
+                             band: tuple = (1.0 / 50.0, 50.0), tail: int = 5) -> ScalingReport:
+    """Barrier-diagonal growth rates over the last ``tail`` iterates (diagnostics.py:271-322).
+
+    Expected by class of the final solution: sigma1 ~ mu, sigma2 ~ 1/mu on
+    positive indices (mirrored on negative ones), both ~ 1/mu on zero
+    indices, lambda1 ~ 1/mu everywhere, sigma1 sigma2 of order one on the
+    active set.  mu is each state's duality measure.  The diagonals and the
+    ratio ranges are computed on the GPU (NumPy or CUDA states).
+    """
+    import torch
+
+    from .newton_system import barrier_diagonals
+
+    if not states:
+        raise ValueError("empty trajectory")
+    window = states[-tail:]
+    if support is None:
+        support = classify_support(window[-1].beta)
+    dev = _dev.device()
+    cls = [torch.as_tensor(np.asarray(a, dtype=np.int64), device=dev)
+           for a in (support.positive, support.negative, support.zero, support.active)]
+    pos, neg, zero, active = cls
+    acc = [[] for _ in range(8)]
+    for st in window:
+        mu = st.duality_measure()
+        d = barrier_diagonals(_dev.to_dev(st.s1), _dev.to_dev(st.s2), _dev.to_dev(st.nu1), _dev.to_dev(st.nu2))
+        s1, s2 = d.sigma1, d.sigma2
+        for i, v in enumerate((d.lambda1 * mu, s1[pos] / mu, s2[pos] * mu, s1[neg] * mu, s2[neg] / mu,
+                               s1[zero] * mu, s2[zero] * mu, s1[active] * s2[active])):
+            acc[i].append(v)
+    ranges = []
+    for chunk in acc:
+        v = torch.cat(chunk)
+        ranges.append((1.0, 1.0) if v.numel() == 0 else (float(v.min()), float(v.max())))
+    lo, hi = band
+    return ScalingReport(band=tuple(band), iterations_checked=len(window), lambda1_times_mu=ranges[0],
+                         sigma1_over_mu_pos=ranges[1], sigma2_times_mu_pos=ranges[2],
+                         sigma1_times_mu_neg=ranges[3], sigma2_over_mu_neg=ranges[4],
+                         sigma1_times_mu_zero=ranges[5], sigma2_times_mu_zero=ranges[6],
+                         sigma_product_active=ranges[7],
+                         in_band=all(lo <= r[0] and r[1] <= hi for r in ranges))

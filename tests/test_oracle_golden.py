@@ -92,3 +92,21 @@ def test_ista_and_soft_threshold_match_reference():
         np.testing.assert_array_equal(beta, g[name + "_beta"])
         assert orc.lasso_objective(beta, g[name + "_b"], m, float(g[name + "_lam"])) == \
             float(g[name + "_objective"])
+
+
+def test_dense_spectrum_probe_matches_reference():
+    """oracle.dense_condensed / preconditioned_spectrum == reference
+    diagnostics.py:94-224 on two observer snapshots of a reference solve."""
+    g = load_golden("spectrum")
+    m = orc.make_mask((24,), missing=g["missing"])
+    fields = ("beta", "z", "s1", "s2", "y1", "y2", "nu1", "nu2")
+    for tag in ("first", "last"):
+        st = orc.OState(*(g[f"{tag}__{f}"] for f in fields), mu=0.0)
+        k, p = orc.dense_condensed(st, m)
+        assert k.tobytes() == g[f"{tag}__K"].tobytes() and p.tobytes() == g[f"{tag}__P"].tobytes()
+        rep = orc.preconditioned_spectrum(st, m)
+        np.testing.assert_array_equal(rep["eigenvalues"], g[f"{tag}__eigs"])
+        sc = g[f"{tag}__scalars"]
+        got = [rep["unit_cluster_size"], rep["predicted_cluster_size"], rep["kappa_observed"], rep["kappa_predicted"],
+               rep["kappa_unpreconditioned"], rep["n_active"], rep["strict_complementarity"], rep["duality_measure"]]
+        np.testing.assert_array_equal(np.array(got, dtype=np.float64), sc)
