@@ -61,6 +61,20 @@ def alg_bytes_per_pass(n: int, ndim: int) -> list[float]:
     return [16.0 * n] * (ndim - 1) + [mid] + [16.0 * n] * (ndim - 1) + [56.0 * n]
 
 
+def bench_config(size: int, world: int) -> dict:
+    """The workload description, identical in both arms (b200 and reference)."""
+    if world <= 1:
+        return {"workload": f"C4: {size}^3 Bragg-punched grid (15.1% missing), one condensed KKT matvec "
+                            "K (d_beta, d_z) per step (newton_system.py:148-152)",
+                "n": size ** 3, "parallelism": "1 GPU",
+                "l2": "inputs 4 GiB per step > 126 MB L2 (no flush needed)"}
+    dims = weak_dims(world, size)
+    return {"workload": f"slab-sharded condensed KKT matvec, global grid {list(dims)} ({size}^3 voxels per "
+                        "GPU, weak scaling), one matvec per step",
+            "n": int(np.prod(dims)), "parallelism": f"slab x{world}",
+            "l2": "inputs 4 GiB per GPU per step > 126 MB L2 (no flush needed)"}
+
+
 def measured_peak_hbm():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -244,29 +258,44 @@ def run_b200(args, rank: int, world: int):
                    "executed_GBps": round(op_bytes / (ms_per_step * 1e6), 1)}
     clock = clocks.summary()
 
-    # e2e: the drop-in call with pinned host direction vectors
+    # e2e (headline): the drop-in call exactly as a reference caller makes it --
+    # NumPy d_beta, d_z and a NumPy BarrierDiagonals (newton_system.py:148-152;
+    # the caller's diag comes from barrier_diagonals(NumPy ...)), so sigma1 and
+    # sigma2 go up every call too: 4n doubles up, 2n down per step.
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    np_db, np_dz = d[:n].cpu().numpy(), d[n:].cpu().numpy()
+    diag_np = BarrierDiagonals(sig1.cpu().numpy(), sig2.cpu().numpy(), None, None, None, None)
+
+    def e2e_run(db_, dz_, diag_, reps):
+        checksum = 0.0
+        for _ in range(2):  # warm the pinned host-allocator cache
+            out_top, out_bot = apply_kkt(db_, dz_, diag_, mask)
+            del out_top, out_bot
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            out_top, out_bot = apply_kkt(db_, dz_, diag_, mask)  # returns host (NumPy) arrays
+            checksum += float(out_top[0]) + float(out_bot[-1])  # consume, then drop
+            del out_top, out_bot
+        barrier()
+        return time.perf_counter() - t0
+
+    e2e_s = e2e_run(np_db, np_dz, diag_np, e2e_steps)
+    e2e = {"value": round(world * e2e_steps / e2e_s, 3), "unit": UNIT,
+           "h2d_bytes_per_step": 4 * n * 8, "d2h_bytes_per_step": 2 * n * 8, "steps": e2e_steps,
+           "api": "newton_system.apply_kkt(NumPy d_beta, NumPy d_z, NumPy BarrierDiagonals, mask) -> NumPy"}
+    del np_db, np_dz, diag_np
+    # secondary: pinned host direction vectors, diagonals already on the device
     diag = BarrierDiagonals(sig1, sig2, None, None, None, None)
     h_db = torch.empty(n, dtype=torch.float64, pin_memory=True)
     h_dz = torch.empty(n, dtype=torch.float64, pin_memory=True)
     h_db.copy_(d[:n])
     h_dz.copy_(d[n:])
-    e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    checksum = 0.0
-    for _ in range(2):  # warm the pinned host-allocator cache
-        out_top, out_bot = apply_kkt(h_db, h_dz, diag, mask)
-        del out_top, out_bot
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        out_top, out_bot = apply_kkt(h_db, h_dz, diag, mask)  # returns host (NumPy) arrays
-        checksum += float(out_top[0]) + float(out_bot[-1])  # consume, then drop
-        del out_top, out_bot
-    barrier()
-    e2e_s = time.perf_counter() - t0
+    e2e_p = e2e_run(h_db, h_dz, diag, e2e_steps)
     del h_db, h_dz
-    e2e = {"value": round(world * e2e_steps / e2e_s, 3), "unit": UNIT,
-           "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": 2 * n * 8,
-           "steps": e2e_steps, "api": "newton_system.apply_kkt(pinned host d_beta, d_z)"}
+    e2e_pinned = {"value": round(world * e2e_steps / e2e_p, 3), "unit": UNIT,
+                  "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": 2 * n * 8, "steps": e2e_steps,
+                  "api": "newton_system.apply_kkt(pinned host d_beta, d_z; device-resident diagonals)"}
 
     del d, top, bot, sig1, sig2
     torch.cuda.empty_cache()
@@ -277,8 +306,9 @@ def run_b200(args, rank: int, world: int):
         other = run_other_solves(barrier)
         if not args.no_c5:
             other["C5 1024^3 Bragg, lambda=0.5, ONE GPU"] = run_c5(barrier)
-    return dict(value=value, ms_per_step=ms_per_step, roofline=roofline, roofline_operator=roofline_op,
-                passes=passes, clocks=clock, e2e=e2e, solve=solve_info, other=other,
+    roofline["operator"] = roofline_op
+    return dict(value=value, ms_per_step=ms_per_step, roofline=roofline,
+                passes=passes, clocks=clock, e2e=e2e, e2e_pinned=e2e_pinned, solve=solve_info, other=other,
                 gpu_launches=args.steps * npass)
 
 
@@ -482,6 +512,11 @@ def run_solve(side: int, barrier):
 
     out = _solve_instance(workloads.c4_const(side), barrier, ista=True)
     out["config"] = f"C4 recipe {side}^3, lambda=0.5, tol=1e-8"
+    # solve-level byte rate, lower bound: only the PCG iterations' traffic
+    # (248 B/voxel each: 5-pass gram + fused update + p-update, DESIGN 4.2)
+    pcg_bytes = out["total_krylov"] * 248.0 * side ** 3
+    out["pcg_bytes_model"] = pcg_bytes
+    out["achieved_GBps_lower_bound"] = round(pcg_bytes / out["device_s"] / 1e9, 1)
     return out
 
 
@@ -580,24 +615,68 @@ def cpu_cores() -> int:
     return max(1, int(cap)) if cap else (os.cpu_count() or 1)
 
 
+def cpu_solve_seconds(inst, reps: int):
+    """Full CPU solves of a recipe instance with the oracle port (the reference's
+    own bench harness times solve() with perf_counter, cli.py:117-122)."""
+    from oracle import fftlasso_oracle as orc
+
+    om = orc.make_mask(inst.dims, flags=inst.flags)
+    b = orc.observe(inst.beta_true, om) + inst.noise
+    times, rep = [], None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _, rep = orc.solve(b, om, orc.OConfig(lam=inst.lam, tol=1e-8))
+        times.append(time.perf_counter() - t0)
+    return {"solve_s": round(statistics.median(times), 4), "runs": reps, "status": rep.status,
+            "ipm_iterations": rep.iterations, "krylov": rep.krylov_counts, "final_objective": rep.final_objective}
+
+
 def run_reference(args):
     times = cpu_matvec_seconds(args.size, args.steps, min(args.warmup, 1), args.ref_budget)
     per = sum(times) / len(times)
     value = 1.0 / per
     sample = (f"{len(times)} of {args.steps} requested steps (time cap {args.ref_budget:.0f} s), "
               f"each one oracle kkt_apply at {args.size}^3; warmup {min(args.warmup, 1)}")
+    solves = {}
+    if not args.no_solve:
+        from paper_2502_04217_b200 import workloads
+
+        for name, mk, reps in (("C1 1D 4096 lambda=0.3", lambda: workloads.c1_1d(seed=0), 3),
+                               ("C2 2048^2 block-punched, default lambda", lambda: workloads.c2_2d(seed=0), 1)):
+            try:
+                solves[name] = cpu_solve_seconds(mk(), reps)
+            except Exception as exc:  # report, never hide
+                solves[name] = {"error": repr(exc)[:300]}
+        solves["C3 256^3 Bragg-punched, default lambda"] = {
+            "not_run": "~8 min of CPU; the reference's own converged solve took 494.7 s on 8 threads "
+                       "(tests/golden/solve_c3_256.json cpu_seconds)"}
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT,
         "n_gpus": args.gpus, "steps": len(times), "warmup": min(args.warmup, 1),
         "ms_per_step": round(per * 1e3, 1), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C4: {args.size}^3 Bragg-punched grid, one condensed KKT matvec per step",
-                   "cpu": "NumPy/SciPy oracle port of fftlasso (reference is pure Python)"},
+        "config": bench_config(args.size, int(os.environ.get("WORLD_SIZE", "1"))),
         "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-                         "sample": sample},
+                         "sample": sample,
+                         "impl": "NumPy/SciPy oracle port of fftlasso (the reference is pure Python and "
+                                 "cannot travel to the GPU box); pocketfft workers = cores"},
         "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_solves": solves, "host": host_info(),
     }
     print(json.dumps(line), flush=True)
+
+
+def host_info() -> dict:
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    info["model"] = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return info
 
 
 def main():
@@ -672,11 +751,10 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms"] / args.steps, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": f"slab-sharded KKT matvec, global grid {res['dims']} "
-                                       f"({args.size}^3 voxels per GPU; P={P}: 5 HBM passes + 2 all-to-all "
-                                       "transposes + epilogue per matvec)",
-                           "n": n_all, "parallelism": f"slab x{P}" + (" (emulated on 1 GPU)" if isinstance(comm, sh.LocalComm) else ""),
-                           "l2": "inputs >> 126 MB L2"},
+                "config": bench_config(args.size, P),
+                "emulated": isinstance(comm, sh.LocalComm),
+                "exchange": "5 HBM passes + 2 slab transposes (peer stores over NVLink, or NCCL all-to-all) "
+                            "+ epilogue per matvec",
                 "roofline": {"bound": "hbm", "achieved": round(120.125 * n_all / P / (res["ms"] / args.steps * 1e6), 1),
                              "peak": peak, "unit": "GB/s",
                              "frac": round(120.125 * n_all / P / (res["ms"] / args.steps * 1e6) / peak, 4),
@@ -697,20 +775,19 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            times = cpu_matvec_seconds(args.size, 1, 0, 60.0)
-            cpu = {"value": round(1.0 / times[0], 5), "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-                   "sample": f"1 oracle kkt_apply at {args.size}^3 (NumPy/SciPy, pocketfft workers={cpu_cores()})"}
+            times = cpu_matvec_seconds(args.size, 2, 1, 60.0)
+            cpu = {"value": round(len(times) / sum(times), 5), "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+                   "sample": f"{len(times)} oracle kkt_apply at {args.size}^3 after 1 warm-up "
+                             f"(NumPy/SciPy, pocketfft workers={cpu_cores()})"}
         line = {
             "metric": METRIC, "value": round(res["value"], 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_per_step"], 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"C4: {args.size}^3 Bragg-punched grid (15.1% missing), one condensed "
-                                   "KKT matvec per step (fused gram: 5 HBM passes + epilogue)",
-                       "n": args.size ** 3, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                       "l2": "inputs 4 GiB per step > 126 MB L2 (no flush needed)"},
-            "roofline": res["roofline"], "roofline_operator": res["roofline_operator"],
-            "passes": res["passes"], "cpu_baseline": cpu, "e2e": res["e2e"], "clocks": res["clocks"],
+            "config": bench_config(args.size, world),
+            "roofline": res["roofline"],
+            "passes": res["passes"], "cpu_baseline": cpu, "e2e": res["e2e"], "e2e_pinned": res["e2e_pinned"],
+            "clocks": res["clocks"],
             "gpu_launches": res["gpu_launches"], "solve": res["solve"], "solves_other_configs": res["other"],
         }
         print(json.dumps(line), flush=True)

@@ -113,6 +113,72 @@ def _upload(a: np.ndarray, dev, out=None):
     return out
 
 
+def upload_chunks(groups, stream):
+    """Host->device copies in order, one CUDA event per group, on ``stream``.
+
+    ``groups`` is a list of lists of (host CPU tensor, device tensor, lo, hi):
+    element range [lo, hi) of the host tensor goes to the same range of the
+    device tensor.  Pinned sources DMA directly; pageable ones (NumPy views)
+    are copied into pinned 64 MiB slots by worker threads while earlier
+    slots are already in flight (a pageable DMA source crawls through the
+    driver's bounce buffer).  Returns the per-group events.
+    """
+    global _pool
+    from concurrent.futures import ThreadPoolExecutor
+
+    if _pool is None:
+        _pool = ThreadPoolExecutor(max_workers=4, thread_name_prefix="fl-upload")
+    step = _UPLOAD_CHUNK // 8
+    pieces = []  # (group index, src, dst, lo, hi), pageable ones split into slots
+    for gi, grp in enumerate(groups):
+        for src, dst, lo, hi in grp:
+            if src.is_pinned():
+                pieces.append((gi, src, dst, lo, hi, None))
+            else:
+                for a in range(lo, hi, step):
+                    pieces.append((gi, src, dst, a, min(hi, a + step), True))
+    nslot = 8
+    slots = [torch.empty(step, dtype=F64, pin_memory=True) for _ in range(nslot)]
+    slot_free = [None] * nslot  # event: the DMA out of the slot has finished
+
+    def fill(k, src, lo, hi, ev):
+        if ev is not None:
+            ev.synchronize()
+        np.copyto(slots[k].numpy()[:hi - lo], src.numpy()[lo:hi])
+
+    events = []
+    futures = {}
+    k = 0
+    # prefetch: queue the fills of the first nslot pageable pieces
+    staged = [i for i, p in enumerate(pieces) if p[5]]
+    order = {i: j % nslot for j, i in enumerate(staged)}
+    for j, i in enumerate(staged[:nslot]):
+        _, src, _, lo, hi, _ = pieces[i]
+        futures[i] = _pool.submit(fill, order[i], src, lo, hi, None)
+    nxt = nslot
+    with torch.cuda.stream(stream):
+        for i, (gi, src, dst, lo, hi, paged) in enumerate(pieces):
+            if paged:
+                k = order[i]
+                futures.pop(i).result()
+                dst[lo:hi].copy_(slots[k][:hi - lo], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                slot_free[k] = ev
+                if nxt < len(staged):  # refill this slot for a later piece
+                    ii = staged[nxt]
+                    _, s2, _, l2, h2, _ = pieces[ii]
+                    futures[ii] = _pool.submit(fill, order[ii], s2, l2, h2, ev)
+                    nxt += 1
+            else:
+                dst[lo:hi].copy_(src[lo:hi], non_blocking=True)
+            if i + 1 == len(pieces) or pieces[i + 1][0] != gi:
+                e = torch.cuda.Event()
+                e.record(stream)
+                events.append(e)
+    return events
+
+
 def empty(n: int):
     return torch.empty(int(n), dtype=F64, device=device())
 

@@ -126,12 +126,15 @@ def _host_tensor(x, n):
 def _apply_kkt_streamed(d_beta, d_z, diag: BarrierDiagonals, mask: Mask):
     """apply_kkt for host inputs: PCIe transfers overlapped with the work.
 
-    d_beta goes up first and the gram runs on it while d_z streams up in
-    chunks; each chunk's epilogue (top needs g and d_z, bottom needs d_beta
-    and d_z) runs as soon as the chunk lands and its results stream back on
-    a third stream, so the device->host traffic overlaps the host->device
-    traffic (PCIe is full duplex).  Same kernels as the device path, results
-    bitwise equal.
+    d_beta goes up first and the gram runs on it while d_z -- and sigma1,
+    sigma2 when the diagonals are host arrays too (a NumPy caller's
+    BarrierDiagonals) -- stream up in chunks; each chunk's epilogue (top
+    needs g, d_z and the sigmas, bottom d_beta, d_z and the sigmas) runs as
+    soon as its inputs land and its results stream back on a third stream,
+    so device->host traffic overlaps host->device traffic (PCIe is full
+    duplex).  Pageable NumPy sources are staged through pinned chunks by
+    worker threads (``_dev.upload_chunks``).  Same kernels as the device
+    path, results bitwise equal.
     """
     import torch
 
@@ -144,30 +147,32 @@ def _apply_kkt_streamed(d_beta, d_z, diag: BarrierDiagonals, mask: Mask):
         _copy_streams[dev.index] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
     h2d, d2h = _copy_streams[dev.index]
     comp = torch.cuda.current_stream()
-    g1, g2 = _vec(diag.sigma1, n), _vec(diag.sigma2, n)
     db, dz, top, bot = (_dev.empty(n) for _ in range(4))
+    sig_host = [not _dev.is_device(x) for x in (diag.sigma1, diag.sigma2)]
+    g1 = _dev.empty(n) if sig_host[0] else _vec(diag.sigma1, n)
+    g2 = _dev.empty(n) if sig_host[1] else _vec(diag.sigma2, n)
     out_t = torch.empty(n, dtype=torch.float64, pin_memory=True)
     out_b = torch.empty(n, dtype=torch.float64, pin_memory=True)
     step = -(-n // _STREAM_CHUNKS)
     step += step % 2  # 16-byte epilogue accesses
     bounds = [(a, min(n, a + step)) for a in range(0, n, step)]
     h2d.wait_stream(comp)  # the device buffers were allocated on the compute stream
-    with torch.cuda.stream(h2d):
-        db.copy_(hb, non_blocking=True)
-        ev_b = torch.cuda.Event()
-        ev_b.record(h2d)
-        ev_z = []
-        for a, b in bounds:
-            dz[a:b].copy_(hz[a:b], non_blocking=True)
-            e = torch.cuda.Event()
-            e.record(h2d)
-            ev_z.append(e)
+    # upload order: all of d_beta (the gram needs it whole), then per chunk
+    # d_z and the host sigmas; one event per (d_beta) and per chunk
+    jobs = [[(hb, db, 0, n)]]
+    for a, b in bounds:
+        grp = [(hz, dz, a, b)]
+        for is_host, src, dst in zip(sig_host, (diag.sigma1, diag.sigma2), (g1, g2)):
+            if is_host:
+                grp.append((_host_tensor(src, n), dst, a, b))
+        jobs.append(grp)
+    events = _dev.upload_chunks(jobs, h2d)
     plan = _dev.plan_for(mask.shape.dims)
     dm = mask.on_device()
-    comp.wait_event(ev_b)
+    comp.wait_event(events[0])
     _lib.call("fl_gram", plan.handle, _dev.ptr(dm.bits), _dev.ptr(db), _dev.ptr(top), _dev.stream())
     sz = 8  # bytes per double
-    for (a, b), e in zip(bounds, ev_z):
+    for (a, b), e in zip(bounds, events[1:]):
         comp.wait_event(e)
         off = a * sz
         _lib.call("fl_kkt_epilogue", b - a, ctypes.c_void_p(top.data_ptr() + off),
@@ -181,7 +186,7 @@ def _apply_kkt_streamed(d_beta, d_z, diag: BarrierDiagonals, mask: Mask):
             out_t[a:b].copy_(top[a:b], non_blocking=True)
             out_b[a:b].copy_(bot[a:b], non_blocking=True)
     d2h.synchronize()
-    for t in (db, dz, top, bot):  # keep the caching allocator stream-safe
+    for t in (db, dz, top, bot, g1, g2):  # keep the caching allocator stream-safe
         t.record_stream(h2d)
         t.record_stream(d2h)
     return out_t.numpy(), out_b.numpy()

@@ -188,17 +188,20 @@ def test_large_grid_matches_oracle(dims):
     assert np.max(np.abs(fl.observe_adjoint(w, mask) - orc.observe_adjoint(w, om))) <= 1e-12 * np.abs(w).max()
 
 
-def test_apply_kkt_streamed_host_path_bitwise(rng):
+@pytest.mark.parametrize("side", [128, 256])
+def test_apply_kkt_streamed_host_path_bitwise(rng, side):
     """Host inputs at n >= 2^20 take the chunked, PCIe-overlapped path: same
     results, bit for bit, as the device-resident call (NumPy and pinned CPU
-    tensors)."""
+    tensors; NumPy BarrierDiagonals as a reference caller passes them).  At
+    256^3 the pageable sources need more pinned staging slots than exist, so
+    slot reuse is exercised."""
     import torch
 
     from paper_2502_04217_b200 import workloads
 
-    dims = (128, 128, 128)
+    dims = (side,) * 3
     shape = fl.GridShape(dims)
-    mask = fl.Mask.from_bool(workloads.bragg_flags(128), shape)
+    mask = fl.Mask.from_bool(workloads.bragg_flags(side), shape)
     n = shape.n
     s = [rng.random(n) + 0.4 for _ in range(4)]
     d = ns.barrier_diagonals(*s)
@@ -211,6 +214,11 @@ def test_apply_kkt_streamed_host_path_bitwise(rng):
     pz = torch.from_numpy(dz).pin_memory()
     t_p, b_p = ns.apply_kkt(pb, pz, d, mask)
     assert t_p.tobytes() == ref_t.tobytes() and b_p.tobytes() == ref_b.tobytes()
+    assert isinstance(d.sigma1, np.ndarray)
+    dd = ns.BarrierDiagonals(*(torch.from_numpy(np.asarray(x)).cuda() for x in
+                               (d.sigma1, d.sigma2, d.lambda1, d.lambda2, d.dvec, d.bvec)))
+    t_m, b_m = ns.apply_kkt(db, dz, dd, mask)  # host directions, device diagonals
+    assert t_m.tobytes() == ref_t.tobytes() and b_m.tobytes() == ref_b.tobytes()
 
 
 def test_large_numpy_upload_exact(rng):
