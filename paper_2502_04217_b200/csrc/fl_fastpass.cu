@@ -19,6 +19,9 @@ Entry make_2048(bool strided, int kind, bool epi);
 Entry make_4096(bool strided, int kind, bool epi);
 Entry make_8192(bool strided, int kind, bool epi);
 Entry make_split_1024(int kind);
+Entry make_group_512(int kind, bool epi);
+Entry make_group_1024(int kind, bool epi);
+Entry make_group_2048(int kind, bool epi);
 
 Entry lookup(int m, bool strided, int kind, bool epi) {
   switch (m) {
@@ -78,7 +81,21 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
   }();
   const bool split = m == 1024 && strided && !epi && (kind == K_SYNTH || kind == K_ANALYZE) &&
                      (split_mode == 2 || (split_mode == 1 && A.inner >= 16384));
-  Entry e = split ? fpk::make_split_1024(kind) : lookup(m, strided, kind, epi);
+  // contiguous m = 512 / 1024 / 2048: group-decoupled passes (fl_gpass.cuh);
+  // they stage rows with TMA, so the row pointers must be 16-byte aligned.
+  // FL_GPASS = 0 falls back to the CTA-tiled engine.
+  static const bool gpass_on = [] {
+    const char* v = std::getenv("FL_GPASS");
+    return !(v && v[0] == '0');
+  }();
+  const bool aligned = (reinterpret_cast<uintptr_t>(A.in) & 15) == 0 &&
+                       (kind != K_RESID || (reinterpret_cast<uintptr_t>(A.bhat) & 15) == 0);
+  const bool group = gpass_on && !strided && aligned && (m == 512 || m == 1024 || m == 2048) &&
+                     (kind == K_SYNTH || kind == K_ANALYZE || kind == K_GRAM || kind == K_RESID);
+  Entry e = split ? fpk::make_split_1024(kind)
+            : group ? (m == 512 ? fpk::make_group_512(kind, epi)
+                       : m == 1024 ? fpk::make_group_1024(kind, epi) : fpk::make_group_2048(kind, epi))
+                    : lookup(m, strided, kind, epi);
   if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");
   int grid_cap = 0, dev = 0;
   FL_CUDA(cudaGetDevice(&dev));
