@@ -226,6 +226,11 @@ FL_API int fl_recover_eliminated(int64_t n, const double* sigma1, const double* 
 /* ---- PCG (pcg.py) ------------------------------------------------------ */
 /* Device work doubles needed by fl_pcg_kkt for a plan of size n. */
 FL_API int64_t fl_pcg_work_doubles(int64_t n);
+/* PCG loop of fl_pcg_kkt / fl_ipm_newton_pcg / fl_ipm_newton_step, process
+ * wide: 3 (default) = one CUDA graph per solve whose WHILE node loops on the
+ * device; 2 = host loop over the same kernels (one sync per iteration).  Both
+ * give bitwise the same iterates (tested); no reference counterpart. */
+FL_API int fl_set_pcg_loop(int mode);
 /* pcg_solve (pcg.py:57-127) on the condensed KKT system K x = rhs
  * (ipm.py:318-327), device resident: fused gram+epilogue matvec, fused
  * update/preconditioner/dot pass, one host sync per iteration.

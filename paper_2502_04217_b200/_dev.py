@@ -71,6 +71,8 @@ def to_dev(x, n: int | None = None, what: str = "vector", scratch=None):
 
 
 _UPLOAD_MIN = 32 << 20
+# host threads filling pinned staging chunks (NumPy releases the GIL in the copy)
+_POOL_WORKERS = 8
 _UPLOAD_CHUNK = 64 << 20
 _pool = None
 _side_streams: dict = {}
@@ -89,7 +91,7 @@ def _upload(a: np.ndarray, dev, out=None):
     from concurrent.futures import ThreadPoolExecutor
 
     if _pool is None:
-        _pool = ThreadPoolExecutor(max_workers=4, thread_name_prefix="fl-upload")
+        _pool = ThreadPoolExecutor(max_workers=_POOL_WORKERS, thread_name_prefix="fl-upload")
     if out is None:
         out = torch.empty(a.size, dtype=F64, device=dev)
     stage = torch.empty(a.size, dtype=F64, pin_memory=True)
@@ -127,7 +129,7 @@ def upload_chunks(groups, stream):
     from concurrent.futures import ThreadPoolExecutor
 
     if _pool is None:
-        _pool = ThreadPoolExecutor(max_workers=4, thread_name_prefix="fl-upload")
+        _pool = ThreadPoolExecutor(max_workers=_POOL_WORKERS, thread_name_prefix="fl-upload")
     step = _UPLOAD_CHUNK // 8
     pieces = []  # (group index, src, dst, lo, hi), pageable ones split into slots
     for gi, grp in enumerate(groups):
@@ -220,7 +222,7 @@ def _download(t):
     from concurrent.futures import ThreadPoolExecutor
 
     if _pool is None:
-        _pool = ThreadPoolExecutor(max_workers=4, thread_name_prefix="fl-upload")
+        _pool = ThreadPoolExecutor(max_workers=_POOL_WORKERS, thread_name_prefix="fl-upload")
     flat = t.reshape(-1)
     res = np.empty(flat.numel(), dtype=np.float64)
     step = _UPLOAD_CHUNK // 8

@@ -76,6 +76,7 @@ SIGNATURES = {
     "fl_precond_apply": (_I, [_I64] + [_P] * 6 + [_P]),
     "fl_newton_rhs": (_I, [_I64, ctypes.POINTER(FlState), _P, _P, _P, _D, _D] + [_P] * 8 + [_P]),
     "fl_recover_eliminated": (_I, [_I64] + [_P] * 12 + [_P]),
+    "fl_set_pcg_loop": (_I, [_I]),
     "fl_pcg_work_doubles": (_I64, [_I64]),
     "fl_pcg_kkt": (_I, [_P] * 7 + [_D, _D, _I64, ctypes.POINTER(FlPcgResult), _P, _I64, _P]),
     "fl_ipm_newton_pcg": (_I, [_P, _P, ctypes.POINTER(FlState), _P, _D, _D, _P, _P, _P, _P, _D, _D, _I64,

@@ -74,24 +74,13 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
   // 512-point halves (fl_split.cuh) wins on the large-stride axis (1024^3
   // axis 0: synthesis 7.44 -> 6.36 ms, analysis 7.43 -> 6.18 ms) and loses on
   // the 8 KiB-stride one (4.98 -> 5.94 ms), so it is chosen by stride.
-  // FL_SPLIT = 0 never, 2 always, default by stride.
-  static const int split_mode = [] {
-    const char* v = std::getenv("FL_SPLIT");
-    return v ? std::atoi(v) : 1;
-  }();
-  const bool split = m == 1024 && strided && !epi && (kind == K_SYNTH || kind == K_ANALYZE) &&
-                     (split_mode == 2 || (split_mode == 1 && A.inner >= 16384));
+  const bool split = m == 1024 && strided && !epi && (kind == K_SYNTH || kind == K_ANALYZE) && A.inner >= 16384;
   // contiguous m = 512 / 1024 / 2048: group-decoupled passes (fl_gpass.cuh);
-  // they stage rows with TMA, so the row pointers must be 16-byte aligned.
-  // FL_GPASS = 0 falls back to the CTA-tiled engine.
-  static const bool gpass_on = [] {
-    const char* v = std::getenv("FL_GPASS");
-    return !(v && v[0] == '0');
-  }();
+  // they stage rows with TMA, so the row pointers must be 16-byte aligned
+  // (an unaligned view falls back to the CTA-tiled engine).
   const bool aligned = (reinterpret_cast<uintptr_t>(A.in) & 15) == 0 &&
                        (kind != K_RESID || (reinterpret_cast<uintptr_t>(A.bhat) & 15) == 0);
-  const bool group = gpass_on && !strided && aligned && (m == 512 || m == 1024 || m == 2048) &&
-                     (kind == K_SYNTH || kind == K_ANALYZE || kind == K_GRAM || kind == K_RESID);
+  const bool group = !strided && aligned && (m == 512 || m == 1024 || m == 2048) && A.G < (1LL << 30);
   Entry e = split ? fpk::make_split_1024(kind)
             : group ? (m == 512 ? fpk::make_group_512(kind, epi)
                        : m == 1024 ? fpk::make_group_1024(kind, epi) : fpk::make_group_2048(kind, epi))

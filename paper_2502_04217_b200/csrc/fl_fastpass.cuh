@@ -251,30 +251,6 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
       }
     }
     double2 v[E];
-    if constexpr (KIND == K_COPY) {
-      // measurement kernel: the same tiles, lanes and loop with the FFT removed
-      if (valid) {
-        const double* px = A.in + Q.bx + (int64_t)q * Q.st;
-        const double* py = A.in + Q.by + (int64_t)q * Q.st;
-        double* ox = A.out + Q.bx + (int64_t)q * Q.st;
-        double* oy = A.out + Q.by + (int64_t)q * Q.st;
-        const int64_t rs = (int64_t)P * Q.st;
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-          if (STRIDED) v[r] = *reinterpret_cast<const double2*>(px + r * rs);
-          else v[r] = make_double2(px[r * rs], Q.by >= 0 ? py[r * rs] : 0.0);
-        }
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-          if (STRIDED) *reinterpret_cast<double2*>(ox + r * rs) = v[r];
-          else {
-            ox[r * rs] = v[r].x;
-            if (Q.by >= 0) oy[r * rs] = v[r].y;
-          }
-        }
-      }
-      continue;
-    }
     if (KIND == K_ANALYZE) {
       if (PIPE > 0) {
 #pragma unroll
@@ -722,142 +698,75 @@ struct Entry {
   int threads = 0, smem = 0, w = 0;
 };
 
-template <int M, bool S, int CFG>
-Entry make_cfg(int kind, bool epi) {
-  Entry e;
-  using G = Geom<M, CFG>;
-  switch (kind) {
-    case K_COPY: e.fn = fast_pass<M, S, K_COPY, false, CFG>; break;
-    case K_SYNTH: e.fn = fast_pass<M, S, K_SYNTH, false, CFG>; break;
-    case K_ANALYZE:
-      e.fn = epi ? fast_pass<M, S, K_ANALYZE, true, CFG> : fast_pass<M, S, K_ANALYZE, false, CFG>;
-      break;
-    case K_GRAM:
-      if constexpr (!S)
-        e.fn = epi ? fast_pass<M, false, K_GRAM, true, CFG> : fast_pass<M, false, K_GRAM, false, CFG>;
-      break;
-    default:
-      if constexpr (!S)
-        e.fn = epi ? fast_pass<M, false, K_RESID, true, CFG> : fast_pass<M, false, K_RESID, false, CFG>;
-      break;
-  }
-  e.threads = G::T;
-  e.smem = G::SMEM + ((kind == K_RESID && !S && G::PIPE == 1) ? G::STAGE_BYTES : 0);
-  e.w = G::W;
-  return e;
-}
-
-// Default variant: plain strided passes on 512-thread CTAs without staging
-// (2 CTAs/SM at 64 registers); the fused gram pass and anything with an
-// epilogue on 256-thread CTAs with single-buffer cp.async staging (tools/
-// sweep_cfg.py on B200: 0.80 ms vs 0.92 double-buffered for the 512^3 gram pass).
+// One kernel per (length, strided, kind, epilogue), no run-time switches.
+// Variant choice (measured in round 1 with per-pass CUDA events, DESIGN 4.1):
+//   * plain strided synthesis / analysis ("light"): the mirrored engine for
+//     m = 64 / 512 / 4096 (fl_mirror.cuh, 256 threads, no staging), else the
+//     E = 8 engine on 512-thread CTAs without staging (2 CTAs/SM);
+//   * everything else at m <= 512: 256-thread CTAs with single-buffer
+//     staging; m >= 1024: the same with one CTA per SM and the full register
+//     budget (E = 16);
+//   * contiguous m = 512 / 1024 / 2048 passes and strided m = 1024 at large
+//     stride are dispatched before this table (fl_gpass.cuh, fl_split.cuh).
 constexpr int kCfgLight = cfg_code(1, 0, 2);
 constexpr int kCfgHeavy = cfg_code(0, 1, 2);
+constexpr int kCfgLong = cfg_code(0, 1, 1);
 
-// Experiment hook (M = 512 only): FL_CFG_STRIDED / FL_CFG_CONTIG pick one of
-// the instantiated variants below for every plain-strided / other pass.
-template <bool S>
-Entry make512(int kind, bool epi, int cfg) {
-  switch (cfg) {
-    case cfg_code(1, 0, 2): return make_cfg<512, S, cfg_code(1, 0, 2)>(kind, epi);
-    case cfg_code(0, 1, 3): return make_cfg<512, S, cfg_code(0, 1, 3)>(kind, epi);
-    case cfg_code(0, 2, 2): return make_cfg<512, S, cfg_code(0, 2, 2)>(kind, epi);
-    case cfg_code(1, 1, 1): return make_cfg<512, S, cfg_code(1, 1, 1)>(kind, epi);
-    case cfg_code(1, 2, 1): return make_cfg<512, S, cfg_code(1, 2, 1)>(kind, epi);
-    case cfg_code(0, 0, 3): return make_cfg<512, S, cfg_code(0, 0, 3)>(kind, epi);
-    case cfg_code(0, 1, 2): return make_cfg<512, S, cfg_code(0, 1, 2)>(kind, epi);
-    case cfg_code(0, 0, 2, 1): return make_cfg<512, S, cfg_code(0, 0, 2, 1)>(kind, epi);
-    case cfg_code(0, 1, 2, 1): return make_cfg<512, S, cfg_code(0, 1, 2, 1)>(kind, epi);
-    case cfg_code(1, 0, 1, 1): return make_cfg<512, S, cfg_code(1, 0, 1, 1)>(kind, epi);
-    default: return Entry();
-  }
-}
-
-inline int env_cfg(const char* name) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : -1;
-}
-
-template <int M, bool S, int PIPE, int MB = 2>
-Entry make_mirror(int kind, bool epi) {
+template <int M, bool S, int CFG>
+Entry entry_of(KernelFn fn) {
   Entry e;
-  using G = mirror::MGeom<M>;
-  switch (kind) {
-    case K_SYNTH: e.fn = mirror_pass<M, S, K_SYNTH, false, PIPE, MB>; break;
-    case K_ANALYZE:
-      e.fn = epi ? mirror_pass<M, S, K_ANALYZE, true, PIPE, MB> : mirror_pass<M, S, K_ANALYZE, false, PIPE, MB>;
-      break;
-    case K_GRAM:
-      if constexpr (!S)
-        e.fn = epi ? mirror_pass<M, false, K_GRAM, true, PIPE, MB> : mirror_pass<M, false, K_GRAM, false, PIPE, MB>;
-      break;
-    case K_RESID:
-      if constexpr (!S)
-        e.fn = epi ? mirror_pass<M, false, K_RESID, true, PIPE, MB> : mirror_pass<M, false, K_RESID, false, PIPE, MB>;
-      break;
-    default: break;
-  }
+  using G = Geom<M, CFG>;
+  e.fn = fn;
   e.threads = G::T;
-  e.smem = G::FIB_BYTES + PIPE * G::STAGE_BYTES;
+  e.smem = G::SMEM;
   e.w = G::W;
   return e;
 }
 
-// FL_MIRROR: 0 off, 1 staging per kind (light passes direct, others single
-// cp.async buffer), 2 no staging, 3 single staging for every kind,
-// 4 (default) plain strided synthesis/analysis only, no staging -- the
-// measured best (tools/sweep_cfg.py); the fused gram pass keeps the E=8 engine;
-// 5/6 as 4 plus the gram/residual pass on the mirrored engine with one
-// 256-thread CTA per SM (255 registers, no spills) and single (5) or no (6)
-// staging.
-inline int mirror_mode() {
-  const char* v = std::getenv("FL_MIRROR");
-  return v ? std::atoi(v) : 4;
+template <int M, bool S, int CFG>
+Entry make_heavy(int kind, bool epi) {
+  using G = Geom<M, CFG>;
+  if (kind == K_SYNTH) return entry_of<M, S, CFG>(fast_pass<M, S, K_SYNTH, false, CFG>);
+  if (kind == K_ANALYZE) {
+    if constexpr (S) return epi ? Entry() : entry_of<M, S, CFG>(fast_pass<M, S, K_ANALYZE, false, CFG>);
+    else return entry_of<M, S, CFG>(epi ? fast_pass<M, S, K_ANALYZE, true, CFG> : fast_pass<M, S, K_ANALYZE, false, CFG>);
+  }
+  if constexpr (!S) {
+    if (kind == K_GRAM)
+      return entry_of<M, S, CFG>(epi ? fast_pass<M, S, K_GRAM, true, CFG> : fast_pass<M, S, K_GRAM, false, CFG>);
+    if (kind == K_RESID) {
+      if (epi) return Entry();  // no caller fuses an epilogue into the residual pass
+      Entry e = entry_of<M, S, CFG>(fast_pass<M, S, K_RESID, false, CFG>);
+      if (G::PIPE == 1) e.smem += G::STAGE_BYTES;  // the staged b_hat rows
+      return e;
+    }
+  }
+  return Entry();
 }
 
 template <int M, bool S>
 Entry make(int kind, bool epi) {
-  const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE || kind == K_COPY);
-  if constexpr (M == 64 || M == 512 || M == 4096) {
-    int mm = kind == K_COPY ? 0 : mirror_mode();
-    if ((mm == 5 || mm == 6) && !light && (kind == K_GRAM || kind == K_RESID)) {
-      if constexpr (M == 512) {
-        Entry e = mm == 5 ? make_mirror<M, S, 1, 1>(kind, epi) : make_mirror<M, S, 0, 1>(kind, epi);
-        if (e.fn) return e;
-      }
-    }
-    if (mm >= 4) mm = light ? 2 : 0;
-    if (mm > 0) {
-      const bool pipe = mm == 3 || (mm == 1 && !light);
-      Entry e = pipe ? make_mirror<M, S, 1>(kind, epi) : make_mirror<M, S, 0>(kind, epi);
-      if (e.fn) return e;
+  const bool light = S && !epi && (kind == K_SYNTH || kind == K_ANALYZE);
+  if constexpr (S && (M == 64 || M == 512 || M == 4096)) {
+    if (light) {
+      using G = mirror::MGeom<M>;
+      Entry e;
+      e.fn = kind == K_SYNTH ? mirror_pass<M, true, K_SYNTH, false, 0> : mirror_pass<M, true, K_ANALYZE, false, 0>;
+      e.threads = G::T;
+      e.smem = G::FIB_BYTES;
+      e.w = G::W;
+      return e;
     }
   }
-  if constexpr (M == 512) {
-    const int over_s = env_cfg("FL_CFG_STRIDED"), over_c = env_cfg("FL_CFG_CONTIG");
-    const int over = light ? over_s : over_c;
-    if (over >= 0) {
-      Entry e = make512<S>(kind, epi, over);
-      if (e.fn) return e;
+  if constexpr (S && M <= 512 && !(M == 64 || M == 512)) {
+    if (light) {
+      return entry_of<M, S, kCfgLight>(kind == K_SYNTH ? fast_pass<M, S, K_SYNTH, false, kCfgLight>
+                                                       : fast_pass<M, S, K_ANALYZE, false, kCfgLight>);
     }
   }
-  if constexpr (M <= 512) {
-    if (light) return make_cfg<M, S, kCfgLight>(kind, epi);
-  }
-  if constexpr (M >= 1024) {
-    // long fibres (E = 16): the fibre tiles fill one CTA per SM anyway (one
-    // staged tile is 138 KB), so ask for one and let the FFT keep ~200
-    // registers: 1024^3 gram 37.2 -> 33.1 ms, 2048^2 0.115 -> 0.100 ms.
-    // FL_CFG_BIG = 1 (256 threads, no staging, 2 CTAs/SM) / 2 (512 threads,
-    // no staging) / 0 (the m <= 512 heavy variant) for comparison.
-    static const int big = env_cfg("FL_CFG_BIG");
-    if (big == 1) return make_cfg<M, S, cfg_code(0, 0, 2)>(kind, epi);
-    if (big == 2) return make_cfg<M, S, cfg_code(1, 0, 1)>(kind, epi);
-    if (big != 0) return make_cfg<M, S, cfg_code(0, 1, 1)>(kind, epi);
-  }
-  return make_cfg<M, S, kCfgHeavy>(kind, epi);
+  if constexpr (M >= 1024) return make_heavy<M, S, kCfgLong>(kind, epi);
+  else return make_heavy<M, S, kCfgHeavy>(kind, epi);
 }
-
 
 template <int M>
 Entry make_any(bool strided, int kind, bool epi) {

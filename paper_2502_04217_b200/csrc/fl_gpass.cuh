@@ -109,24 +109,26 @@ __global__ void __launch_bounds__(GCfg<M>::T, GCfg<M>::MINB) group_pass(const Pa
   const bool leader = tg == 0;
   const double2* tw = A.plan.tw;
   const double c0 = A.c0, c1 = A.c1;
-  const int64_t gstride = (int64_t)gridDim.x * NG;
-  int64_t g = (int64_t)blockIdx.x * NG + c;
+  // pair indices fit 32 bits (the launcher falls back to the CTA-tiled engine otherwise)
+  const int gstride = (int)gridDim.x * NG;
+  const int npairs = (int)A.G;
+  int g = (int)blockIdx.x * NG + c;
   if (leader) {
     fast::mbar_init(bar, 1);
     fast::mbar_init(bar + 1, 1);
   }
   __syncthreads();
-  if (leader && g < A.G) tma_rows<M>(A.in, geo<false>(A, g), stage, bar);
+  if (leader && g < npairs) tma_rows<M>(A.in, geo<false>(A, g), stage, bar);
   unsigned ph0 = 0, ph1 = 0;
   int buf = 0;
   double acc = 0.0, nrm = 0.0;
-  for (; g < A.G; g += gstride) {
+  for (; g < npairs; g += gstride) {
     const Geo Q = geo<false>(A, g);
-    const int64_t gn = g + gstride;
+    const int gn = g + gstride;
     const bool has_y = Q.by >= 0;
     // refill of the stage with the next pair's rows (after the stage's last read)
     auto refill_next = [&]() {
-      if (leader && gn < A.G) tma_rows<M>(A.in, geo<false>(A, gn), stage, bar);
+      if (leader && gn < npairs) tma_rows<M>(A.in, geo<false>(A, gn), stage, bar);
     };
     fast::mbar_wait(bar, ph0);
     ph0 ^= 1u;
@@ -314,7 +316,7 @@ fpk::Entry make_group(int kind, bool epi) {
     case K_SYNTH: e.fn = group_pass<M, K_SYNTH, false>; break;
     case K_ANALYZE: e.fn = epi ? group_pass<M, K_ANALYZE, true> : group_pass<M, K_ANALYZE, false>; break;
     case K_GRAM: e.fn = epi ? group_pass<M, K_GRAM, true> : group_pass<M, K_GRAM, false>; break;
-    case K_RESID: e.fn = epi ? group_pass<M, K_RESID, true> : group_pass<M, K_RESID, false>; break;
+    case K_RESID: e.fn = epi ? nullptr : group_pass<M, K_RESID, false>; break;  // no caller fuses an epilogue here
     default: break;
   }
   e.threads = GCfg<M>::T;

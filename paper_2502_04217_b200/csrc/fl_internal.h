@@ -34,7 +34,7 @@ namespace fl {
 
 constexpr int kMaxDevices = 16;  // per-device caches (scratch, kernel attributes)
 
-enum PassKind : int { K_SYNTH = 0, K_ANALYZE = 1, K_GRAM = 2, K_RESID = 3, K_COPY = 4 };
+enum PassKind : int { K_SYNTH = 0, K_ANALYZE = 1, K_GRAM = 2, K_RESID = 3 };
 
 struct KktEpi {
   const double* pb = nullptr;   // d_beta
@@ -73,13 +73,6 @@ int kkt_epilogue(int64_t n, double* g, const double* pb, const double* pz, const
                  const double* sig2, double* bottom, double* partials, int* nblocks, cudaStream_t s);
 
 // PCG kernels (fl_vec.cu)
-int pcg_init(int64_t n, const double* sig1, const double* sig2, const double* rhs, double* x,
-             double* r, double* p, double* partials, int* nblocks, cudaStream_t s);
-int pcg_update(int64_t n, const double* sig1, const double* sig2, const double* rho,
-               const double* curv, double* x, double* r, const double* p, const double* kp_top,
-               const double* kp_bot, double* partials, int* nblocks, cudaStream_t s);
-int pcg_pupdate(int64_t n, const double* sig1, const double* sig2, const double* r, double beta,
-                double* p, cudaStream_t s);
 // restructured PCG: curvature = ||Z A p_beta||^2 (fused gram pass) + diagonal form
 int pcg2_init(int64_t n, const double* sig1, const double* sig2, const double* rhs, double* x, double* r,
               double* p, double* partials, int* nblocks, cudaStream_t s);

@@ -8,6 +8,7 @@
 // Scalar recurrences (alpha, beta, the stopping test, breakdown checks)
 // follow pcg.py exactly, in IEEE double.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -435,86 +436,11 @@ int pcg_v3(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double
 }
 
 
-// v1: materialised K p (gram + elementwise epilogue with d.Kd partials), then
-// a fused update pass reading K p; kept behind FL_PCG_V1=1 for comparison.
-int pcg_v1(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2, const double* rhs,
-           double* x, double* work, double abs_tol, double rel_tol, int64_t max_iters, fl_pcg_result* res,
-           double* history, int64_t max_history, cudaStream_t s) {
-  const int64_t n = p->n;
-  double* r = work;
-  double* pv = work + 2 * n;
-  double* kt = work + 4 * n;
-  double* kb = work + 5 * n;
-  double* slots = work + 6 * n;  // [rho_a, rho_b, curv]
-  Scratch* sc;
-  FL_TRY(scratch(&sc));
-  const int64_t limit = max_iters >= 0 ? max_iters : std::min<int64_t>(10 * 2 * n, kPcgIterCap);
-  const int ksum = RED_SUM;
-  History record{history, max_history};
-  int nb = 0;
-  FL_TRY(pcg_init(n, sigma1, sigma2, rhs, x, r, pv, sc->partials, &nb, s));
-  FL_TRY(finish_reduce(sc->partials, nb, 1, &ksum, slots, s));
-  FL_CUDA(cudaMemcpyAsync(sc->host, slots, sizeof(double), cudaMemcpyDeviceToHost, s));
-  FL_CUDA(cudaStreamSynchronize(s));
-  double rho = sc->host[0];
-  FL_TRY(check_rho(rho, 0));
-  const double norm0 = std::sqrt(rho);
-  const double thr = abs_tol + rel_tol * norm0;
-  record(norm0);
-  res->norm0 = norm0;
-  if (norm0 <= thr) {
-    res->iterations = 0;
-    res->converged = 1;
-    res->residual_norm = norm0;
-    return FL_OK;
-  }
-  double norm = norm0;
-  int cur = 0;
-  KktEpi e;
-  e.pb = pv;
-  e.pz = pv + n;
-  e.sig1 = sigma1;
-  e.sig2 = sigma2;
-  e.bottom = kb;
-  e.partials = sc->partials;
-  for (int64_t k = 1; k <= limit; ++k) {
-    int nbk = 0, nbu = 0;
-    FL_TRY(op_gram(p, bits, nullptr, false, pv, kt, &e, &nbk, s));
-    FL_TRY(finish_reduce(sc->partials, nbk, 1, &ksum, slots + 2, s));
-    FL_TRY(pcg_update(n, sigma1, sigma2, slots + cur, slots + 2, x, r, pv, kt, kb, sc->partials, &nbu, s));
-    FL_TRY(finish_reduce(sc->partials, nbu, 1, &ksum, slots + (1 - cur), s));
-    FL_CUDA(cudaMemcpyAsync(sc->host, slots, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    FL_CUDA(cudaStreamSynchronize(s));
-    FL_TRY(check_curv(sc->host[2], k));
-    const double rho_next = sc->host[1 - cur];
-    FL_TRY(check_rho(rho_next, k));
-    norm = std::sqrt(rho_next);
-    record(norm);
-    if (norm <= thr) {
-      res->iterations = k;
-      res->converged = 1;
-      res->residual_norm = norm;
-      return FL_OK;
-    }
-    FL_TRY(pcg_pupdate(n, sigma1, sigma2, r, rho_next / rho, pv, s));
-    rho = rho_next;
-    cur = 1 - cur;
-  }
-  res->iterations = limit;
-  res->converged = 0;
-  res->residual_norm = norm;
-  return FL_OK;
-}
-
-int pcg_mode() {
-  static const int mode = [] {
-    const char* e = std::getenv("FL_PCG");  // 1: v1, 2: v2 (host loop), default 3 (graph loop)
-    const char* v1 = std::getenv("FL_PCG_V1");
-    if (v1 && v1[0] == '1') return 1;
-    return e ? std::atoi(e) : 3;
-  }();
-  return mode;
-}
+// PCG loop: 3 = one CUDA graph with a device WHILE loop per solve (default),
+// 2 = host loop of the same kernels (one sync per iteration).  Set through
+// fl_set_pcg_loop (tests compare the two bit for bit).
+std::atomic<int> g_pcg_mode{3};
+int pcg_mode() { return g_pcg_mode.load(std::memory_order_relaxed); }
 
 int64_t pcg_limit(int64_t n, int64_t max_iters) {
   return max_iters >= 0 ? max_iters : std::min<int64_t>(10 * 2 * n, kPcgIterCap);
@@ -537,6 +463,12 @@ extern "C" {
 
 int64_t fl_pcg_work_doubles(int64_t n) { return 6 * n + 16; }
 
+int fl_set_pcg_loop(int mode) {
+  if (mode != 2 && mode != 3) return fail(FL_E_VALUE, "PCG loop mode must be 2 (host) or 3 (device graph)");
+  g_pcg_mode.store(mode, std::memory_order_relaxed);
+  return FL_OK;
+}
+
 int fl_pcg_kkt(fl_plan_t p, const uint32_t* bits, const double* sigma1, const double* sigma2,
                const double* rhs, double* x, double* work, double abs_tol, double rel_tol,
                int64_t max_iters, fl_pcg_result* res, double* history, int64_t max_history,
@@ -548,8 +480,6 @@ int fl_pcg_kkt(fl_plan_t p, const uint32_t* bits, const double* sigma1, const do
   const int64_t limit = pcg_limit(p->n, max_iters);
   const int mode = pcg_mode();
   cudaStream_t s = (cudaStream_t)stream;
-  if (mode == 1) return pcg_v1(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, limit, res, history,
-                               max_history, s);
   if (mode == 3 && !(history && max_history > 0))
     return pcg_v3(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, limit, res, s);
   return pcg_v2(p, bits, sigma1, sigma2, rhs, x, work, abs_tol, rel_tol, limit, res, history, max_history, s);

@@ -222,8 +222,7 @@ int fl_analyze(fl_plan_t p, const double* x, double* beta, fl_stream_t stream) {
 int fl_axis_pass(fl_plan_t p, int axis, int analysis, const double* in, double* out, fl_stream_t stream) {
   if (!p || !in || !out) return fail(FL_E_VALUE, "null argument");
   if (axis < 0 || axis >= p->ndim) return fail(FL_E_VALUE, "axis out of range");
-  // analysis == 2: tile-copy measurement kernel (same tiles/lanes, no FFT; power-of-two axes)
-  const int kind = analysis == 2 ? K_COPY : (analysis ? K_ANALYZE : K_SYNTH);
+  const int kind = analysis ? K_ANALYZE : K_SYNTH;
   return run_pass(p, axis, kind, in, out, nullptr, nullptr, nullptr, nullptr, (cudaStream_t)stream);
 }
 

@@ -537,59 +537,6 @@ __global__ void k_xpby(int64_t n, const double* __restrict__ x, double beta, dou
 
 // ---------------- PCG on the condensed system (pcg.py:84-127) ----------------
 // 2n vectors are [beta-block (n); z-block (n)].
-__global__ void k_pcg_init(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
-                           const double* __restrict__ rhs, double* __restrict__ x,
-                           double* __restrict__ r, double* __restrict__ p,
-                           double* __restrict__ partials) {
-  __shared__ double red[32];
-  double rho = 0.0;
-  GRID_LOOP(i, n) {
-    const double rb = rhs[i], rc = rhs[n + i];
-    const Pinv P(g1[i], g2[i]);
-    const double zt = P.top(rb, rc), zb = P.bot(rb, rc);
-    x[i] = 0.0;
-    x[n + i] = 0.0;
-    r[i] = rb;
-    r[n + i] = rc;
-    p[i] = zt;
-    p[n + i] = zb;
-    rho += mul(rb, zt) + mul(rc, zb);
-  }
-  emit(rho, SumOp(), red, partials, 0);
-}
-
-__global__ void k_pcg_update(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
-                             const double* __restrict__ rho_p, const double* __restrict__ curv_p,
-                             double* __restrict__ x, double* __restrict__ r,
-                             const double* __restrict__ p, const double* __restrict__ kt,
-                             const double* __restrict__ kb, double* __restrict__ partials) {
-  __shared__ double red[32];
-  const double alpha = dvd(*rho_p, *curv_p);
-  double rho = 0.0;
-  GRID_LOOP(i, n) {
-    const double pt = p[i], pb = p[n + i];
-    x[i] = add(x[i], mul(alpha, pt));
-    x[n + i] = add(x[n + i], mul(alpha, pb));
-    const double rt = sub(r[i], mul(alpha, kt[i]));
-    const double rb = sub(r[n + i], mul(alpha, kb[i]));
-    r[i] = rt;
-    r[n + i] = rb;
-    const Pinv P(g1[i], g2[i]);
-    rho += mul(rt, P.top(rt, rb)) + mul(rb, P.bot(rt, rb));
-  }
-  emit(rho, SumOp(), red, partials, 0);
-}
-
-__global__ void k_pcg_pupdate(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
-                              const double* __restrict__ r, double beta, double* __restrict__ p) {
-  GRID_LOOP(i, n) {
-    const double rt = r[i], rb = r[n + i];
-    const Pinv P(g1[i], g2[i]);
-    p[i] = add(P.top(rt, rb), mul(beta, p[i]));
-    p[n + i] = add(P.bot(rt, rb), mul(beta, p[n + i]));
-  }
-}
-
 // KKT epilogue (newton_system.py:150-151) on the gram output g, in place:
 // top = (g + L1 pb) + L2 pz, bottom = L2 pb + L1 pz, partial d.Kd.  16-byte
 // accesses (n is even for every grid).
@@ -825,25 +772,6 @@ int reduce_fetch(Scratch* sc, int grid, int nk, const int* kinds, double* out, c
 }  // namespace
 
 // ---- internal entry points used by the PCG driver ----
-int pcg_init(int64_t n, const double* sig1, const double* sig2, const double* rhs, double* x,
-             double* r, double* p, double* partials, int* nblocks, cudaStream_t s) {
-  const int grid = grid_for(n, T);
-  k_pcg_init<<<grid, T, 0, s>>>(n, sig1, sig2, rhs, x, r, p, partials);
-  FL_LAUNCH_CHECK();
-  *nblocks = grid;
-  return FL_OK;
-}
-
-int pcg_update(int64_t n, const double* sig1, const double* sig2, const double* rho,
-               const double* curv, double* x, double* r, const double* p, const double* kp_top,
-               const double* kp_bot, double* partials, int* nblocks, cudaStream_t s) {
-  const int grid = grid_for(n, T);
-  k_pcg_update<<<grid, T, 0, s>>>(n, sig1, sig2, rho, curv, x, r, p, kp_top, kp_bot, partials);
-  FL_LAUNCH_CHECK();
-  *nblocks = grid;
-  return FL_OK;
-}
-
 int kkt_epilogue(int64_t n, double* g, const double* pb, const double* pz, const double* sig1,
                  const double* sig2, double* bottom, double* partials, int* nblocks, cudaStream_t s) {
   const int64_t n2 = n / 2;
@@ -901,13 +829,6 @@ int dot_partials(int64_t n, const double* a, const double* b, double* partials, 
   k_dot<<<grid, T, 0, s>>>(n, a, b, partials);
   FL_LAUNCH_CHECK();
   *nblocks = grid;
-  return FL_OK;
-}
-
-int pcg_pupdate(int64_t n, const double* sig1, const double* sig2, const double* r, double beta,
-                double* p, cudaStream_t s) {
-  k_pcg_pupdate<<<grid_for(n, T), T, 0, s>>>(n, sig1, sig2, r, beta, p);
-  FL_LAUNCH_CHECK();
   return FL_OK;
 }
 

@@ -20,7 +20,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import os
 import time
 from dataclasses import dataclass
 
@@ -486,10 +485,10 @@ def _fused_step(prob: Problem, ws: Workspace, mu: float, lam: float, config: Ipm
     return res, alpha_p, alpha_d
 
 
-# FL_IPM_ASYNC=0 selects the step with a host sync after each stage
-# (_fused_step); the default issues the whole step with one sync (the
-# assessment's), same kernels in the same order, bitwise the same iterates.
-_ASYNC_STEP = os.environ.get("FL_IPM_ASYNC", "1") != "0"
+# True (default): the whole step is issued with one sync (the assessment's);
+# False: a host sync after each stage (_fused_step) -- same kernels in the
+# same order, bitwise the same iterates (tests flip this attribute).
+_ASYNC_STEP = True
 
 
 def _launch_step(prob: Problem, ws: Workspace, mu: float, lam: float, config: IpmConfig) -> None:

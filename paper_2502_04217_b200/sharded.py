@@ -27,7 +27,7 @@ works on *lists of local shards* (length 1 under DistComm, P under
 LocalComm).
 
 Two exchange implementations (``ShardedGrid(..., exchange=...)``, default
-from ``FL_SHARD_EXCHANGE``):
+``"peer"``):
 
 * ``"peer"`` (default; falls back to ``"a2a"`` if peer buffers cannot be
   set up): ONE kernel per direction stores every element, transposed,
@@ -379,14 +379,15 @@ class ShardOps:
 class ShardedGrid:
     """Geometry, comm, per-shard ops and exchange buffers of one sharded grid."""
 
-    def __init__(self, dims, comm: Comm, ops_factory=ShardOps, exchange=None):
-        import os
-
+    def __init__(self, dims, comm: Comm, ops_factory=ShardOps, exchange=None, chunks=None):
         self.geo = SlabGeometry(tuple(int(d) for d in dims), comm.world)
         self.comm = comm
         self.ops = [ops_factory(self.geo) for _ in comm.ranks]
         n = self.geo.n_local
-        self.exchange = exchange or os.environ.get("FL_SHARD_EXCHANGE", "peer")
+        # forward exchange in plane chunks overlapped with the X-side passes:
+        # default 4 with two or more real ranks, off on one GPU
+        self.chunks = chunks
+        self.exchange = exchange or "peer"
         if self.exchange not in ("a2a", "peer"):
             raise ValueError(f"unknown exchange {self.exchange!r}")
         if self.exchange == "peer":
@@ -442,11 +443,10 @@ class ShardedGrid:
         Default: 4 chunks with two or more ranks (the NVLink stores overlap the
         next chunk's passes); off for one rank / LocalComm, where both compete
         for the same SMs and HBM (measured: 194 -> 187 matvecs/s at 512^3, P = 1).
-        ``FL_SHARD_CHUNKS`` overrides; the chunked path is tested in emulation.
+        ``ShardedGrid(chunks=K)`` overrides; the chunked path is tested in emulation.
         """
-        import os
-
-        K = int(os.environ.get("FL_SHARD_CHUNKS", "4" if isinstance(self.comm, DistComm) and self.comm.world > 1 else "1"))
+        K = self.chunks if self.chunks is not None else (
+            4 if isinstance(self.comm, DistComm) and self.comm.world > 1 else 1)
         a = self.geo.a
         if self.exchange != "peer" or K <= 1 or a % K or not hasattr(self.ops[0], "synth_x_planes"):
             return False
@@ -824,3 +824,117 @@ def _sharded_pcg(grid: ShardedGrid, prob: ShardedProblem, ws, cfg: PcgConfig):
             dq_parts.append(out.value)
         rho = rho_next
     raise NumericalBreakdownError(f"PCG stalled at preconditioned residual {norm:.3e} after {limit} iterations")
+
+
+# ---------------------------------------------------------------------------
+# drop-in entry: solve(b, mask, config, observer) over slab-sharded ranks
+# ---------------------------------------------------------------------------
+
+def default_comm() -> Comm:
+    """DistComm over the default process group when torch.distributed is
+    initialised (one rank per GPU), else a single local shard."""
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return DistComm(device=_dev.device() if dist.get_backend() == "nccl" else None)
+    except Exception:  # pragma: no cover - torch.distributed unavailable
+        pass
+    return LocalComm(1)
+
+
+def _y_inputs(geo: SlabGeometry, flags: np.ndarray, b_hat: np.ndarray, r: int):
+    """Rank r's Y-slab mask bits and b_hat (host transposes of the full grid)."""
+    return pack_bits(geo.y_slab(flags.astype(np.uint8), r)), geo.y_slab(b_hat, r)
+
+
+def solve(b, mask, config: IpmConfig = IpmConfig(), observer=None, comm: Comm | None = None, root: int = 0):
+    """``ipm.solve`` (reference ipm.py:402-486) over P slab-sharded GPUs.
+
+    The reference's calling convention on the ``root`` rank: ``b`` the
+    observed samples (NumPy, n_observed) and ``mask`` a 3D ``Mask`` (or
+    ``BraggMask``); the other ranks pass ``None`` for both.  Root embeds b on
+    the full grid, cuts every rank's Y-slab (axis 0 local and contiguous) of
+    b_hat and of the mask, and ships them over the process group (NCCL
+    point-to-point on B200s); every rank then runs ``sharded_solve`` on its
+    slabs (5 HBM passes + 2 slab exchanges per gram, one all-reduce per
+    scalar decision).  The default penalty 0.1 max|M^T b| (ipm.py:204-206)
+    comes from one sharded residual pass at beta = 0.
+
+    Returns ``(beta, report)`` on root -- beta gathered into one NumPy vector
+    (X-slabs are contiguous chunks of the global vector) -- and
+    ``(None, report)`` elsewhere; the report is identical on every rank.
+    """
+    import torch
+
+    comm = comm or default_comm()
+    dist_mode = isinstance(comm, DistComm)
+    me = comm.ranks[0]
+    is_root = (not dist_mode) or me == root
+    if is_root:
+        if mask.shape.ndim != 3:
+            raise UnsupportedShapeError("the sharded solver takes 3D grids")
+        meta = [tuple(mask.shape.dims), config]
+    else:
+        meta = [None, None]
+    if dist_mode:
+        comm.dist.broadcast_object_list(meta, src=root, group=comm.group)
+    dims, config = meta
+    if config.lam is not None and config.lam <= 0:
+        raise ValueError("penalty must be positive")
+    grid = ShardedGrid(dims, comm)
+    geo = grid.geo
+    nl = geo.n_local
+    dev = _dev.device()
+    bits, bhat = {}, {}
+    if is_root:
+        flags = np.asarray(mask.missing_bool, dtype=bool).reshape(-1)
+        bv = b.detach().cpu().numpy() if _dev.is_device(b) else np.asarray(b, dtype=np.float64).reshape(-1)
+        if bv.size != int((~flags).sum()):
+            raise UnsupportedShapeError(f"observed vector has {bv.size} entries, expected {int((~flags).sum())}")
+        b_hat = np.zeros(geo.n)
+        b_hat[~flags] = bv
+        targets = range(geo.P) if dist_mode else comm.ranks
+        for r in targets:
+            wb, yb = _y_inputs(geo, flags, b_hat, r)
+            tb = torch.from_numpy(wb).to(dev)
+            ty = torch.from_numpy(yb).to(dev)
+            if dist_mode and r != me:
+                comm.dist.send(tb, dst=r, group=comm.group)
+                comm.dist.send(ty, dst=r, group=comm.group)
+            else:
+                bits[r], bhat[r] = tb, ty
+        del b_hat
+    else:
+        tb = torch.empty((nl + 31) // 32, dtype=torch.int32, device=dev)
+        ty = torch.empty(nl, dtype=torch.float64, device=dev)
+        comm.dist.recv(tb, src=root, group=comm.group)
+        comm.dist.recv(ty, src=root, group=comm.group)
+        bits[me], bhat[me] = tb, ty
+    prob = ShardedProblem(grid, [bits[r] for r in comm.ranks], [bhat[r] for r in comm.ranks])
+    lam = config.lam
+    if lam is None:  # default_penalty: 0.1 max|A^T Z b_hat| from one residual pass at beta = 0
+        zs = [_dev.zeros(nl) for _ in comm.ranks]
+        gs = [_dev.empty(nl) for _ in comm.ranks]
+        grid.gram(zs, gs, prob.bits_y, prob.bhat_y)
+        loc = []
+        for g in gs:
+            m = ctypes.c_double()
+            _lib.call("fl_max_abs", nl, _dev.ptr(g), ctypes.byref(m), _dev.stream())
+            loc.append([m.value])
+        lam = 0.1 * float(comm.reduce(loc, MAX)[0])
+        del zs, gs
+        if lam <= 0:
+            raise ValueError("penalty must be positive")
+    betas, report = sharded_solve(prob, lam, config, observer)
+    out = None
+    if dist_mode:
+        parts = [torch.empty(nl, dtype=torch.float64, device=dev) for _ in range(geo.P)] if me == root else None
+        comm.dist.gather(betas[0].contiguous(), gather_list=parts, dst=root, group=comm.group)
+        if me == root:
+            out = torch.cat(parts).cpu().numpy()
+    else:
+        out = geo.from_x([t.cpu().numpy() for t in betas])
+    if hasattr(comm, "release_peer_buffers"):
+        comm.release_peer_buffers()
+    return out, report

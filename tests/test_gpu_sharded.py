@@ -121,14 +121,13 @@ def test_sharded_solve_peer_exchange_equals_a2a():
     assert res["a2a"] == res["peer"]
 
 
-def test_overlapped_forward_exchange_bitwise(monkeypatch):
+def test_overlapped_forward_exchange_bitwise():
     """synth_x + X->Y exchange in plane chunks on two streams == one shot."""
     dims = (64, 32, 48)
     out = {}
-    for k in ("1", "4"):
-        monkeypatch.setenv("FL_SHARD_CHUNKS", k)
+    for k in (1, 4):
         comm = sh.LocalComm(2)
-        grid = sh.ShardedGrid(dims, comm, exchange="peer")
+        grid = sh.ShardedGrid(dims, comm, exchange="peer", chunks=k)
         geo = grid.geo
         beta = np.random.default_rng(5).standard_normal(geo.n)
         flags = np.random.default_rng(6).random(geo.n) < 0.15
@@ -137,14 +136,13 @@ def test_overlapped_forward_exchange_bitwise(monkeypatch):
         g = [fl._dev.empty(geo.n_local) for _ in comm.ranks]
         nrm = grid.gram(xb, g, prob.bits_y, want_norm=True)
         out[k] = (nrm, b"".join(t.cpu().numpy().tobytes() for t in g))
-    assert out["1"] == out["4"]
+    assert out[1] == out[4]
 
 
 def test_sharded_solve_8_ranks_c4_recipe_64():
     """The C5 configuration's rank count (P = 8, peer exchange, chunked
     forward overlap forced on) on the C4 recipe at 64^3 against the
     single-GPU solve."""
-    import os
 
     from paper_2502_04217_b200 import workloads
 
@@ -153,15 +151,11 @@ def test_sharded_solve_8_ranks_c4_recipe_64():
     mask = fl.Mask.from_bool(inst.flags, shape)
     b = fl.observe(inst.beta_true, mask) + inst.noise
     beta1, rep1 = fl.solve(b, mask, fl.IpmConfig(lam=inst.lam))
-    os.environ["FL_SHARD_CHUNKS"] = "2"
-    try:
-        grid = sh.ShardedGrid(inst.dims, sh.LocalComm(8), exchange="peer")
-        bhat = np.zeros(shape.n)
-        bhat[~inst.flags] = b
-        prob = sh.ShardedProblem.from_host(grid, inst.flags, bhat)
-        betas, rep = sh.sharded_solve(prob, inst.lam, fl.IpmConfig(lam=inst.lam))
-    finally:
-        del os.environ["FL_SHARD_CHUNKS"]
+    grid = sh.ShardedGrid(inst.dims, sh.LocalComm(8), exchange="peer", chunks=2)
+    bhat = np.zeros(shape.n)
+    bhat[~inst.flags] = b
+    prob = sh.ShardedProblem.from_host(grid, inst.flags, bhat)
+    betas, rep = sh.sharded_solve(prob, inst.lam, fl.IpmConfig(lam=inst.lam))
     beta = grid.geo.from_x([t.cpu().numpy() for t in betas])
     assert rep.status == rep1.status == "converged" and rep.iterations == rep1.iterations
     assert all(abs(x - y) <= 1 for x, y in zip(rep.krylov_counts, rep1.krylov_counts))
@@ -239,3 +233,49 @@ def test_sharded_solve_8_ranks_device_inputs_256():
     assert np.linalg.norm(beta - b1) <= 1e-8 * np.linalg.norm(b1)
     found = sh.gather_support(betas, geo, grid.comm)
     np.testing.assert_array_equal(found, np.sort(idx))
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_dropin_solve_matches_single_gpu(P):
+    """sharded.solve(b, mask, config): the reference calling convention
+    (NumPy b, Mask, default lambda) over P emulated ranks == fl.solve."""
+    from paper_2502_04217_b200 import workloads
+
+    inst = workloads.c3_bragg(32, seed=0)
+    mask = fl.Mask.from_bool(inst.flags, fl.GridShape(inst.dims))
+    b = fl.observe(inst.beta_true, mask) + inst.noise
+    beta1, rep1 = fl.solve(b, mask, fl.IpmConfig(tol=1e-8))
+    beta, rep = sh.solve(b, mask, fl.IpmConfig(tol=1e-8), comm=sh.LocalComm(P))
+    assert isinstance(beta, np.ndarray) and beta.shape == beta1.shape
+    assert abs(rep.lam - rep1.lam) <= 1e-12 * rep1.lam
+    assert rep.status == rep1.status == "converged" and rep.iterations == rep1.iterations
+    assert all(abs(x - y) <= 1 for x, y in zip(rep.krylov_counts, rep1.krylov_counts))
+    assert abs(rep.final_objective - rep1.final_objective) <= 1e-9 * abs(rep1.final_objective)
+    assert np.linalg.norm(beta - beta1) <= 1e-8 * np.linalg.norm(beta1)
+
+
+def test_sharded_dropin_solve_nccl_world_size_one():
+    """The DistComm route (object broadcast, NCCL gather) at world size 1."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_04217_b200 import workloads
+
+    inst = workloads.c4_const(32)
+    mask = fl.Mask.from_bool(inst.flags, fl.GridShape(inst.dims))
+    b = fl.observe(inst.beta_true, mask) + inst.noise
+    beta1, rep1 = fl.solve(b, mask, fl.IpmConfig(lam=inst.lam))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        beta, rep = sh.solve(b, mask, fl.IpmConfig(lam=inst.lam))
+    finally:
+        dist.destroy_process_group()
+    assert rep.krylov_counts == rep1.krylov_counts
+    assert abs(rep.final_objective - rep1.final_objective) <= 1e-9 * abs(rep1.final_objective)
+    assert np.linalg.norm(beta - beta1) <= 1e-8 * np.linalg.norm(beta1)

@@ -220,74 +220,44 @@ def test_ipm_step_and_check_convergence_match_oracle(rng):
     assert c.centrality_ok == oc["centrality_ok"]
 
 
-def test_pcg_v1_matches_v2():
-    """The materialised-Kp PCG (FL_PCG_V1=1) and the default fused-curvature PCG agree."""
-    import os
-    import subprocess
-    import sys
+def _golden_solves(names):
+    import hashlib
 
-    from conftest import REPO
+    out = {}
+    for name in names:
+        g = load_golden("solve_" + name)
+        dims = tuple(int(d) for d in g["dims"])
+        mi = 3 if name == "maxit_64" else 200
+        beta, rep = fl.solve(g["b"], fl.Mask(g["missing"], fl.GridShape(dims)),
+                             fl.IpmConfig(lam=float(g["lam"]), max_iters=mi))
+        recs = [[r.mu, r.alpha_primal, r.alpha_dual, r.krylov_iters, r.pcg_residual, r.kkt_max]
+                for r in rep.records]
+        out[name] = [rep.status, recs, rep.final_objective, hashlib.sha1(beta.tobytes()).hexdigest()]
+    return out
 
-    code = r'''
-import sys, json, numpy as np
-sys.path.insert(0, %r); sys.path.insert(0, %r)
-import paper_2502_04217_b200 as fl
-from conftest import load_golden
-out = {}
-for name in ("c1_4096", "c3_32", "harm_16"):
-    g = load_golden("solve_" + name)
-    dims = tuple(int(d) for d in g["dims"])
-    beta, rep = fl.solve(g["b"], fl.Mask(g["missing"], fl.GridShape(dims)), fl.IpmConfig(lam=float(g["lam"])))
-    out[name] = [rep.krylov_counts, rep.final_objective, beta.tolist()[:64]]
-print(json.dumps(out))
-''' % (REPO, REPO + "/tests")
+
+GOLDEN_SOLVES = ("c1_4096", "c2_256", "c3_32", "harm_16", "empty_128", "maxit_64")
+
+
+@pytest.fixture
+def pcg_loop():
+    """Select the PCG loop (fl_set_pcg_loop) for one test, restore the default."""
+    from paper_2502_04217_b200 import _lib
+
+    yield lambda mode: _lib.call("fl_set_pcg_loop", mode)
+    _lib.call("fl_set_pcg_loop", 3)
+
+
+def test_pcg_graph_loop_bitwise_equals_host_loop(pcg_loop):
+    """Loop 3 (default: one CUDA graph with a device WHILE loop per PCG
+    solve) runs the same kernels and scalar recurrences as loop 2 (host
+    loop, one sync per iteration): identical records and bitwise identical
+    solutions."""
     res = {}
-    for v1 in ("0", "1"):
-        env = dict(os.environ, FL_PCG_V1=v1)
-        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-        assert out.returncode == 0, out.stderr[-2000:]
-        res[v1] = json.loads(out.stdout.strip().splitlines()[-1])
-    for name in res["0"]:
-        k0, o0, b0 = res["0"][name]
-        k1, o1, b1 = res["1"][name]
-        assert all(abs(a - b) <= 1 for a, b in zip(k0, k1))
-        assert abs(o0 - o1) <= 1e-9 * abs(o1)
-        assert np.allclose(b0, b1, atol=1e-7)
-
-
-def test_pcg_graph_loop_bitwise_equals_host_loop():
-    """FL_PCG=3 (default: one CUDA graph with a device WHILE loop per PCG
-    solve) runs the same kernels and scalar recurrences as FL_PCG=2 (host
-    loop, one sync per iteration): identical Krylov counts and bitwise
-    identical solutions."""
-    import os
-    import subprocess
-    import sys
-
-    from conftest import REPO
-
-    code = r'''
-import sys, json, hashlib, numpy as np
-sys.path.insert(0, %r); sys.path.insert(0, %r)
-import paper_2502_04217_b200 as fl
-from conftest import load_golden
-out = {}
-for name in ("c1_4096", "c2_256", "c3_32", "harm_16", "empty_128", "maxit_64"):
-    g = load_golden("solve_" + name)
-    dims = tuple(int(d) for d in g["dims"])
-    mi = 3 if name == "maxit_64" else 200
-    lam = float(g["lam"])
-    beta, rep = fl.solve(g["b"], fl.Mask(g["missing"], fl.GridShape(dims)), fl.IpmConfig(lam=lam, max_iters=mi))
-    out[name] = [rep.krylov_counts, [r.pcg_residual for r in rep.records], hashlib.sha1(beta.tobytes()).hexdigest()]
-print(json.dumps(out))
-''' % (REPO, REPO + "/tests")
-    res = {}
-    for mode in ("2", "3"):
-        env = dict(os.environ, FL_PCG=mode)
-        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-        assert out.returncode == 0, out.stderr[-2000:]
-        res[mode] = json.loads(out.stdout.strip().splitlines()[-1])
-    assert res["2"] == res["3"]
+    for mode in (2, 3):
+        pcg_loop(mode)
+        res[mode] = _golden_solves(GOLDEN_SOLVES)
+    assert res[2] == res[3]
 
 
 def test_pcg_graph_loop_breakdown_and_cap():
@@ -364,43 +334,19 @@ def test_fused_newton_front_half_bitwise():
                       1e-12, 0.0, 5000, ctypes.byref(out), _dev.stream())
 
 
-def test_one_sync_step_bitwise_equals_synchronous_step():
-    """FL_IPM_ASYNC=1 (default: fl_ipm_newton_step, step lengths and the gated
-    update on the device, one host sync per IPM iteration) == FL_IPM_ASYNC=0
-    (a sync after the PCG, the ratios and the update): identical records and
-    bitwise identical solutions, with the graph PCG loop and the host loop."""
-    import os
-    import subprocess
-    import sys
-
-    from conftest import REPO
-
-    code = r'''
-import sys, json, hashlib, numpy as np
-sys.path.insert(0, %r); sys.path.insert(0, %r)
-import paper_2502_04217_b200 as fl
-from conftest import load_golden
-out = {}
-for name in ("c1_4096", "c2_256", "c3_32", "harm_16", "empty_128", "maxit_64"):
-    g = load_golden("solve_" + name)
-    dims = tuple(int(d) for d in g["dims"])
-    mi = 3 if name == "maxit_64" else 200
-    beta, rep = fl.solve(g["b"], fl.Mask(g["missing"], fl.GridShape(dims)),
-                         fl.IpmConfig(lam=float(g["lam"]), max_iters=mi))
-    recs = [[r.mu, r.alpha_primal, r.alpha_dual, r.krylov_iters, r.pcg_residual, r.kkt_max]
-            for r in rep.records]
-    out[name] = [rep.status, recs, rep.final_objective, hashlib.sha1(beta.tobytes()).hexdigest()]
-print(json.dumps(out))
-''' % (REPO, REPO + "/tests")
+def test_one_sync_step_bitwise_equals_synchronous_step(pcg_loop, monkeypatch):
+    """The one-sync step (default: fl_ipm_newton_step, step lengths and the
+    gated update on the device, one host sync per IPM iteration) == the
+    staged step (a sync after the PCG, the ratios and the update): identical
+    records and bitwise identical solutions, with both PCG loops."""
     res = {}
-    for mode in ("0", "1"):
-        for pcg in ("2", "3"):
-            env = dict(os.environ, FL_IPM_ASYNC=mode, FL_PCG=pcg)
-            out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
-                                 timeout=600)
-            assert out.returncode == 0, out.stderr[-2000:]
-            res[mode + pcg] = json.loads(out.stdout.strip().splitlines()[-1])
-    assert res["03"] == res["13"] == res["02"] == res["12"]
+    for async_step in (False, True):
+        monkeypatch.setattr(ipm, "_ASYNC_STEP", async_step)
+        for mode in (2, 3):
+            pcg_loop(mode)
+            res[(async_step, mode)] = _golden_solves(GOLDEN_SOLVES)
+    first = res[(False, 2)]
+    assert all(v == first for v in res.values())
 
 
 def test_one_sync_step_cap_skips_update():

@@ -1,141 +1,79 @@
-"""GPU: every instantiated pass-kernel variant agrees with the oracle.
+"""GPU: every pass-kernel family of the library agrees with the oracle on
+multi-tile grids (each persistent CTA / group walks several tiles).
 
-Covers 512-long axes in both layouts (the C4/C5 hot path) and other
-power-of-two lengths, for synthesis, analysis and the fused gram, under each
-kernel configuration selectable through FL_CFG_STRIDED / FL_CFG_CONTIG
-(csrc/fl_fastpass.cu), plus the generic engine (FL_FORCE_GENERIC is read once
-per process, so it is exercised in a subprocess).
+One kernel per (length, layout, kind) -- no run-time switches -- so the
+families are reached through the grid shape: the mirrored engine (strided
+m = 64 / 512 / 4096), the E = 8 engine (other strided lengths <= 256, all
+contiguous lengths outside the group set), the group-decoupled contiguous
+passes (m = 512 / 1024 / 2048, fl_gpass.cuh), the long-fibre E = 16 engine
+and the radix-2 split (strided m = 1024, chosen by stride), the generic
+mixed-radix engine (non-power-of-two even lengths) and the four-step path
+(lengths above 8192).
 """
-
-import os
-import subprocess
-import sys
 
 import numpy as np
 import pytest
 
-from conftest import REPO
 from oracle import fftlasso_oracle as orc
 
 pytestmark = pytest.mark.gpu
 
 fl = pytest.importorskip("paper_2502_04217_b200")
+from paper_2502_04217_b200 import _dev, _lib  # noqa: E402
+from paper_2502_04217_b200.masking import embed  # noqa: E402
 
-VARIANTS = [10, 5, 7, 12, 15, 2, 4, 28, 31, 36]
-# the last two give every persistent CTA several tiles (exercises the
-# cross-tile cp.async pipelining)
-DIMS = [(512, 4, 8), (4, 6, 512), (16, 512), (512, 2, 64), (2, 512, 16), (512, 128, 64),
-        (64, 128, 512)]
-
-
-def _mask(dims, rng):
-    n = int(np.prod(dims))
-    return rng.random(n) < 0.15
-
-
-@pytest.mark.parametrize("var", VARIANTS)
-@pytest.mark.parametrize("which", ["FL_CFG_STRIDED", "FL_CFG_CONTIG"])
-def test_variant_matches_oracle(var, which, monkeypatch):
-    monkeypatch.setenv(which, str(var))
-    _check_all_dims(var)
+DIMS = [
+    # m = 512 both layouts (C4), several tiles per persistent CTA / group
+    (512, 4, 8), (4, 6, 512), (16, 512), (512, 2, 64), (2, 512, 16), (512, 128, 64), (64, 128, 512),
+    # mirrored m = 64 / 4096 strided, E = 8 lengths, group m = 1024 / 2048 contiguous
+    (64, 8, 16), (8, 4096), (4096, 4), (64, 64, 64), (256, 32, 256), (32, 128, 128),
+    (4, 1024), (6, 2048), (2, 8, 1024),
+    # strided m = 1024: E = 16 engine (small stride) and radix-2 split (stride >= 16384)
+    (1024, 8, 16), (8, 1024, 24), (1024, 1024), (1024, 4, 4096),
+    # generic mixed-radix and four-step
+    (24, 36), (6, 10, 4), (96, 40, 24), (16384,), (2, 16384),
+]
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "2", "3", "4", "5", "6"])
-def test_mirror_engine_matches_oracle(mode, monkeypatch):
-    """The mirrored-butterfly engine (FL_MIRROR, m = 64 / 512 / 4096)."""
-    monkeypatch.setenv("FL_MIRROR", mode)
-    _check_all_dims(int(mode) + 100)
-    for dims in [(64, 8, 16), (4096,), (8, 4096), (64, 64, 64), (4096, 4)]:
-        _check_dims(dims, np.random.default_rng(len(dims)))
-
-
-def _check_all_dims(seed):
-    rng = np.random.default_rng(seed)
-    for dims in DIMS:
-        _check_dims(dims, rng)
-
-
-def _check_dims(dims, rng):
+@pytest.mark.parametrize("dims", DIMS)
+def test_pass_families_match_oracle(dims):
+    rng = np.random.default_rng(sum(dims))
     shape = fl.GridShape(dims)
-    flags = _mask(dims, rng)
+    flags = rng.random(shape.n) < 0.15
     mask = fl.Mask.from_bool(flags, shape)
     om = orc.make_mask(dims, flags=flags)
     beta = rng.standard_normal(shape.n)
     x = rng.standard_normal(shape.n)
     tol = 1e-12 * max(1.0, np.abs(beta).max())
-    assert np.max(np.abs(fl.synthesize(beta, shape) - orc.synthesize(beta, dims))) <= tol, dims
-    assert np.max(np.abs(fl.analyze(x, shape) - orc.analyze(x, dims))) <= tol, dims
-    assert np.max(np.abs(fl.gram(beta, mask) - orc.gram(beta, om))) <= tol, dims
+    assert np.max(np.abs(fl.synthesize(beta, shape) - orc.synthesize(beta, dims))) <= tol
+    assert np.max(np.abs(fl.analyze(x, shape) - orc.analyze(x, dims))) <= tol
+    assert np.max(np.abs(fl.gram(beta, mask) - orc.gram(beta, om))) <= tol
     w = rng.standard_normal(mask.n_observed)
     ref = orc.observe_adjoint(w, om)
-    assert np.max(np.abs(fl.observe_adjoint(w, mask) - ref)) <= 1e-12 * max(1.0, np.abs(ref).max()), dims
+    assert np.max(np.abs(fl.observe_adjoint(w, mask) - ref)) <= 1e-12 * max(1.0, np.abs(ref).max())
+    # residual pass A^T Z (b_hat - A beta), the solver's data correlation
+    ref_r = orc.observe_adjoint(w - orc.observe(beta, om), om)
+    bh = _dev.to_dev(embed(w, mask))
+    bd = _dev.to_dev(beta)
+    g = _dev.empty(shape.n)
+    _lib.call("fl_residual_adjoint", _dev.plan_for(dims).handle, _dev.ptr(mask.on_device().bits), _dev.ptr(bh),
+              _dev.ptr(bd), _dev.ptr(g), _dev.stream())
+    assert np.max(np.abs(g.cpu().numpy() - ref_r)) <= 1e-12 * max(1.0, np.abs(ref_r).max())
 
 
-def test_generic_engine_matches_oracle():
-    code = r'''
-import sys, numpy as np
-sys.path.insert(0, %r)
-import paper_2502_04217_b200 as fl
-from oracle import fftlasso_oracle as orc
-rng = np.random.default_rng(5)
-for dims in [(512, 4, 8), (4, 6, 512), (64, 32), (24, 36), (6, 10, 4)]:
-    shape = fl.GridShape(dims)
-    flags = rng.random(shape.n) < 0.15
-    m, om = fl.Mask.from_bool(flags, shape), orc.make_mask(dims, flags=flags)
-    b = rng.standard_normal(shape.n)
-    assert np.max(np.abs(fl.synthesize(b, shape) - orc.synthesize(b, dims))) <= 1e-12 * np.abs(b).max(), dims
-    assert np.max(np.abs(fl.gram(b, m) - orc.gram(b, om))) <= 1e-12 * np.abs(b).max(), dims
-print("ok")
-''' % REPO
-    env = dict(os.environ, FL_FORCE_GENERIC="1")
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+def test_kkt_apply_epilogue_families(rng):
+    """KKT epilogue: separate 16-byte pass (2D/3D) and fused into the
+    contiguous gram pass (1D, group and E = 8 engines)."""
+    from paper_2502_04217_b200 import newton_system as ns
 
-
-def test_fused_epilogue_matches_split():
-    code = r'''
-import sys, numpy as np
-sys.path.insert(0, %r)
-import paper_2502_04217_b200 as fl
-from paper_2502_04217_b200 import newton_system as ns
-from oracle import fftlasso_oracle as orc
-rng = np.random.default_rng(6)
-for dims in [(512, 4, 8), (64, 64), (4096,)]:
-    shape = fl.GridShape(dims)
-    flags = rng.random(shape.n) < 0.15
-    m, om = fl.Mask.from_bool(flags, shape), orc.make_mask(dims, flags=flags)
-    s = [rng.random(shape.n) + 0.4 for _ in range(4)]
-    d, od = ns.barrier_diagonals(*s), orc.diagonals(*s)
-    db, dz = rng.standard_normal(shape.n), rng.standard_normal(shape.n)
-    t, b = ns.apply_kkt(db, dz, d, m)
-    ot, ob = orc.kkt_apply(db, dz, od, om)
-    assert np.max(np.abs(t - ot)) <= 1e-11, dims
-    assert np.array_equal(b, ob), dims
-print("ok")
-''' % REPO
-    env = dict(os.environ, FL_FUSED_EPI="1")
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
-
-
-@pytest.mark.parametrize("split", ["0", "2"])
-def test_split_1024_engine_matches_oracle(split):
-    """Strided m = 1024 passes with and without the radix-2 split into two
-    mirrored 512-point halves (FL_SPLIT is read once per process)."""
-    code = r'''
-import sys, numpy as np
-sys.path.insert(0, %r)
-import paper_2502_04217_b200 as fl
-from oracle import fftlasso_oracle as orc
-rng = np.random.default_rng(11)
-for dims in [(1024, 8, 16), (8, 1024, 24), (1024, 1024)]:
-    beta = rng.standard_normal(int(np.prod(dims)))
-    tol = 1e-12 * np.abs(beta).max()
-    sh = fl.GridShape(dims)
-    assert np.max(np.abs(fl.synthesize(beta, sh) - orc.synthesize(beta, dims))) <= tol, dims
-    assert np.max(np.abs(fl.analyze(beta, sh) - orc.analyze(beta, dims))) <= tol, dims
-print("OK")
-''' % REPO
-    env = dict(os.environ, FL_SPLIT=split)
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
+    for dims in [(512, 4, 8), (64, 64), (4096,), (512,), (1024,), (96,)]:
+        shape = fl.GridShape(dims)
+        flags = rng.random(shape.n) < 0.15
+        m, om = fl.Mask.from_bool(flags, shape), orc.make_mask(dims, flags=flags)
+        s = [rng.random(shape.n) + 0.4 for _ in range(4)]
+        d, od = ns.barrier_diagonals(*s), orc.diagonals(*s)
+        db, dz = rng.standard_normal(shape.n), rng.standard_normal(shape.n)
+        t, b = ns.apply_kkt(db, dz, d, m)
+        ot, ob = orc.kkt_apply(db, dz, od, om)
+        assert np.max(np.abs(t - ot)) <= 1e-11, dims
+        assert np.array_equal(b, ob), dims

