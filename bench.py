@@ -301,15 +301,59 @@ def run_b200(args, rank: int, world: int):
     torch.cuda.empty_cache()
     solve_info = None
     other = None
+    passes_1024 = None
     if not args.no_solve:
         solve_info = run_solve(args.solve_size, barrier)
         other = run_other_solves(barrier)
         if not args.no_c5:
             other["C5 1024^3 Bragg, lambda=0.5, ONE GPU"] = run_c5(barrier)
+            try:  # the C5 axis length: per-pass table of one 1024^3 matvec
+                passes_1024 = per_pass_table(1024)
+            except Exception as exc:  # report, never hide
+                passes_1024 = {"error": repr(exc)[:300]}
     roofline["operator"] = roofline_op
     return dict(value=value, ms_per_step=ms_per_step, roofline=roofline,
                 passes=passes, clocks=clock, e2e=e2e, e2e_pinned=e2e_pinned, solve=solve_info, other=other,
+                passes_1024=passes_1024,
                 gpu_launches=args.steps * npass)
+
+
+def per_pass_table(side: int, reps: int = 5):
+    """Per-pass CUDA-event times of one KKT matvec at side^3 (fl_kkt_apply_profiled),
+    device-resident inputs, Bragg mask built on the device."""
+    import ctypes
+
+    import torch
+
+    import paper_2502_04217_b200 as fl
+    from paper_2502_04217_b200 import _dev, _lib
+    from paper_2502_04217_b200.masking import BraggMask
+
+    n = side ** 3
+    shape = fl.GridShape((side,) * 3)
+    dm = BraggMask(shape).on_device()
+    plan = _dev.plan_for(shape.dims)
+    sig1, sig2, d = make_kkt_inputs(side, seed=7)
+    top, bot = _dev.empty(n), _dev.empty(n)
+    buf = (ctypes.c_double * 8)()
+    cnt = ctypes.c_int()
+    acc = np.zeros(6)
+    for i in range(reps + 2):
+        _lib.call("fl_kkt_apply_profiled", plan.handle, _dev.ptr(dm.bits), _dev.ptr(sig1), _dev.ptr(sig2),
+                  _dev.ptr(d[:n]), _dev.ptr(d[n:]), _dev.ptr(top), _dev.ptr(bot), buf, ctypes.byref(cnt),
+                  _dev.stream())
+        if i >= 2:
+            acc += np.array(buf[:6])
+    ms = acc / reps
+    peak, _ = measured_peak_hbm()
+    alg = alg_bytes_per_pass(n, 3)
+    del sig1, sig2, d, top, bot, dm
+    torch.cuda.empty_cache()
+    return {"size": side, "matvec_ms": round(float(ms.sum()), 3), "matvec_per_s": round(1e3 / float(ms.sum()), 2),
+            "operator_frac": round(120.125 * n / (float(ms.sum()) * 1e6) / peak, 4),
+            "passes": [{"name": PASS_NAMES_3D[i], "ms": round(float(ms[i]), 4),
+                        "GBps": round(alg[i] / ms[i] / 1e6, 1), "frac": round(alg[i] / ms[i] / 1e6 / peak, 4)}
+                       for i in range(6)]}
 
 
 def weak_dims(world: int, side: int = 512):
@@ -789,6 +833,7 @@ def main():
             "passes": res["passes"], "cpu_baseline": cpu, "e2e": res["e2e"], "e2e_pinned": res["e2e_pinned"],
             "clocks": res["clocks"],
             "gpu_launches": res["gpu_launches"], "solve": res["solve"], "solves_other_configs": res["other"],
+            "passes_1024": res["passes_1024"],
         }
         print(json.dumps(line), flush=True)
     if world > 1:
