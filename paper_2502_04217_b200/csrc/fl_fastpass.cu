@@ -20,7 +20,7 @@ Entry make_4096(bool strided, int kind, bool epi);
 Entry make_8192(bool strided, int kind, bool epi);
 Entry make_split_1024(int kind);
 Entry make_group_512(int kind, bool epi);
-Entry make_group_1024(int kind, bool epi);
+Entry make_warp_1024(int kind, bool epi);
 Entry make_group_2048(int kind, bool epi);
 
 Entry lookup(int m, bool strided, int kind, bool epi) {
@@ -80,10 +80,14 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
   // (an unaligned view falls back to the CTA-tiled engine).
   const bool aligned = (reinterpret_cast<uintptr_t>(A.in) & 15) == 0 &&
                        (kind != K_RESID || (reinterpret_cast<uintptr_t>(A.bhat) & 15) == 0);
-  const bool group = !strided && aligned && (m == 512 || m == 1024 || m == 2048) && A.G < (1LL << 30);
+  const bool group = !strided && aligned && (m == 512 || m == 2048) && A.G < (1LL << 30);
+  // contiguous m = 1024: the two-stage warp-owned passes (fl_wpass.cuh, one
+  // exchange per FFT; 1024^3 gram 5.61 -> 4.74 ms).  At m = 512 they lose to
+  // the group passes (255 registers leave 8 warps per SM: 1.07 vs 0.65 ms).
+  const bool warp = !strided && m == 1024;
   Entry e = split ? fpk::make_split_1024(kind)
-            : group ? (m == 512 ? fpk::make_group_512(kind, epi)
-                       : m == 1024 ? fpk::make_group_1024(kind, epi) : fpk::make_group_2048(kind, epi))
+            : warp ? fpk::make_warp_1024(kind, epi)
+            : group ? (m == 512 ? fpk::make_group_512(kind, epi) : fpk::make_group_2048(kind, epi))
                     : lookup(m, strided, kind, epi);
   if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");
   int grid_cap = 0, dev = 0;

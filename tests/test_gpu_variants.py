@@ -5,7 +5,8 @@ One kernel per (length, layout, kind) -- no run-time switches -- so the
 families are reached through the grid shape: the mirrored engine (strided
 m = 64 / 512 / 4096), the E = 8 engine (other strided lengths <= 256, all
 contiguous lengths outside the group set), the group-decoupled contiguous
-passes (m = 512 / 1024 / 2048, fl_gpass.cuh), the long-fibre E = 16 engine
+passes (m = 512 / 2048, fl_gpass.cuh), the two-stage warp passes (contiguous
+m = 1024, fl_wpass.cuh), the long-fibre E = 16 engine
 and the radix-2 split (strided m = 1024, chosen by stride), the generic
 mixed-radix engine (non-power-of-two even lengths) and the four-step path
 (lengths above 8192).

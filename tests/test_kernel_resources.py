@@ -21,17 +21,17 @@ LIB = os.path.join(REPO, "paper_2502_04217_b200", "libfftlasso_b200.so")
 HOT = [
     r"mirror_passILi512ELb1ELi[01]ELb0",   # strided m = 512 synthesis / analysis
     r"group_passILi512ELi[012]E",          # contiguous m = 512: synth, analysis, fused gram
-    r"group_passILi1024ELi[0123]E",        # contiguous m = 1024 (C5 axes)
+    r"warp_passILi1024ELi[012]E",          # contiguous m = 1024 (C5 axes): synth, analysis, fused gram
     r"split_pass",                         # strided m = 1024, large stride
     r"fast_passILi1024ELb1ELi[01]ELb0",    # strided m = 1024, small stride (E = 16)
     r"k_kkt_epilogue", r"k_pcg2", r"k_newton_setup", r"k_update", r"k_assess", r"k_ratios",
 ]
 # known spills, all off the BASELINE hot path: small strided lengths on
 # 512-thread CTAs (grids with an axis <= 256), the 8192-long contiguous fused
-# passes (1D 8192 only), the m = 512 residual pass (once per IPM iteration,
-# 8 bytes), the Bragg mask builder's 2-entry extent array.
+# passes (1D 8192 only), the m = 512 and m = 1024 residual passes (once per
+# IPM iteration, 8 / 16 bytes), the Bragg mask builder's 2-entry extent array.
 ALLOWED = [r"fast_passILi(16|32|64|128|256)ELb1", r"fast_passILi8192ELb0", r"group_passILi512ELi3E",
-           r"k_bragg_bits"]
+           r"warp_passILi1024ELi3E", r"k_bragg_bits"]
 
 
 def _resources():
