@@ -98,12 +98,10 @@ __device__ __forceinline__ void dftn(double2* v, int sign) {
 
 // v[k * STRIDE] *= w_M^(sign * base * k), k = 1..N-1 (N <= 32), from five
 // table powers: w^(base k) = w^(4 base m) w^(base l) for k = 4m + l, each
-// factor at most two products from a table entry (~3 ulp).
+// factor at most two products from a table entry (~3 ulp).  The bases are
+// loop invariant; the compiler keeps what it can of the powers across pairs.
 template <int M, int N, int STRIDE>
 __device__ __forceinline__ void twiddle_run(double2* v, int base, const double2* tw, int sign) {
-  // the bases are loop invariant: laundering the table pointer keeps the
-  // compiler from hoisting 24 registers of powers out of the pair loop
-  asm volatile("" : "+l"(tw));
   double2 p1[4], p4[8];
   p1[0] = make_double2(1.0, 0.0);
   p1[1] = twiddle(tw, base, sign);
@@ -211,15 +209,78 @@ __global__ void __launch_bounds__(WG<M>::T, WG<M>::MINB) warp_pass(const PassArg
     const bool has_y = Q.by >= 0;
     const double* rx = A.in + Q.bx;
     const double* ry = A.in + Q.by;
+    {  // L2 prefetch of the warp's next rows (one 128-byte line per lane and step)
+      const int64_t gn = gw + gstride;
+      if (gn < npairs) {
+        const Geo Qn = geo<false>(A, gn);
+        const int64_t nrows = (npairs - gn) < G::PPW ? (npairs - gn) : G::PPW;
+        const char* base = reinterpret_cast<const char*>(A.in + Qn.bx);
+        const int64_t bytes = (Qn.by >= 0 ? 2 : 1) * nrows * M * 8;
+        for (int64_t off = (int64_t)lane * 128; off < bytes; off += 32 * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+      }
+    }
+    // mask words of the pair (one x and one y word per lane), loaded before the
+    // rows so both latencies overlap; the bits are extracted after the unpack
     uint32_t mx = 0, my = 0;
+    uint32_t wxl = 0, wyl = 0;
     if constexpr (MASKED) {
-      // after the inverse FFT slot (j, k2) holds element (q + P j) + 32 k2: word k2, bit q + P j
-      const int wl = lane - lbase;  // one x word and one y word per lane of the pair
-      uint32_t wxl = 0, wyl = 0;
+      const int wl = lane - lbase;
       if (valid && wl < P) {
         wxl = __ldg(A.bits + (Q.bx >> 5) + wl);
         if (has_y) wyl = __ldg(A.bits + (Q.by >> 5) + wl);
       }
+    }
+    double2 v[E];
+    if constexpr (KIND == K_ANALYZE) {
+      // load straight into the split layout the forward FFT starts from:
+      // slot (j, b) = element (q + P j) + 32 b (coalesced along the row)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+          const int t = (q + P * j) + 32 * b;
+          v[j * P + b] = valid ? make_double2(rx[t], has_y ? ry[t] : 0.0) : make_double2(0.0, 0.0);
+        }
+    } else {
+      // unpack: each packed row value is read once; Zin_k (k < H) stays, Zin_{M-k} goes
+      // to the mirror slot (thread P - q, slot 31 - r; thread 0: its own slot 32 - r)
+      double2 hi[E / 2];
+#pragma unroll
+      for (int r = 0; r < E / 2; ++r) {
+        const int k = q + P * r;
+        const bool edge = q0 && r == 0;
+        const int ia = edge ? 0 : k + 1, ib = edge ? 1 : k + H;
+        double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+        if (valid) {
+          ax = rx[ia];
+          bx = rx[ib];
+          if (has_y) {
+            ay = ry[ia];
+            by = ry[ib];
+          }
+        }
+        if (edge) {
+          v[0] = make_double2(c0 * ax, c0 * ay);
+          hi[0] = make_double2(c0 * bx, c0 * by);  // Zin_H -> thread 0 slot E/2
+        } else {
+          v[r] = make_double2(c1 * (ax - by), c1 * (bx + ay));
+          hi[r] = make_double2(c1 * (ax + by), c1 * (ay - bx));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < E / 2; ++r) {
+        const double2 rv = shfl2(hi[r], partner);
+        v[E - 1 - r] = rv;  // thread q >= 1: partner's slot r mirrors our slot 31 - r
+      }
+      if (q0) {  // thread 0 is its own partner: slot 32 - r <- hi[r], slot 16 <- Zin_H
+        v[E / 2] = hi[0];
+#pragma unroll
+        for (int r = 1; r < E / 2; ++r) v[E - r] = hi[r];
+      }
+    }
+    if constexpr (MASKED) {
+      // after the inverse FFT slot (j, k2) holds element (q + P j) + 32 k2: word k2, bit q + P j
       if constexpr (P == 32) {
         // 32 x 32 bit transpose by ballot: bit k2 of ballot qt = bit qt of word k2
 #pragma unroll
@@ -242,50 +303,6 @@ __global__ void __launch_bounds__(WG<M>::T, WG<M>::MINB) warp_pass(const PassArg
             my |= ((wy >> (q + P * j)) & 1u) << (j * P + k2);
           }
         }
-      }
-    }
-    double2 v[E];
-    if constexpr (KIND == K_ANALYZE) {
-      // load straight into the split layout the forward FFT starts from:
-      // slot (j, b) = element (q + P j) + 32 b (coalesced along the row)
-#pragma unroll
-      for (int j = 0; j < NJ; ++j)
-#pragma unroll
-        for (int b = 0; b < P; ++b) {
-          const int t = (q + P * j) + 32 * b;
-          v[j * P + b] = valid ? make_double2(rx[t], has_y ? ry[t] : 0.0) : make_double2(0.0, 0.0);
-        }
-    } else {
-      // unpack: each packed row value is read once; Zin_k (k < H) stays, Zin_{M-k} goes
-      // to the mirror slot (thread P - q, slot 31 - r; thread 0: its own slot 32 - r)
-#pragma unroll
-      for (int r = 0; r < E / 2; ++r) {
-        const int k = q + P * r;
-        const bool edge = q0 && r == 0;
-        const int ia = edge ? 0 : k + 1, ib = edge ? 1 : k + H;
-        double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
-        if (valid) {
-          ax = rx[ia];
-          bx = rx[ib];
-          if (has_y) {
-            ay = ry[ia];
-            by = ry[ib];
-          }
-        }
-        double2 hi;
-        if (edge) {
-          v[0] = make_double2(c0 * ax, c0 * ay);
-          hi = make_double2(c0 * bx, c0 * by);  // Zin_H -> thread 0 slot E/2
-        } else {
-          v[r] = make_double2(c1 * (ax - by), c1 * (bx + ay));
-          hi = make_double2(c1 * (ax + by), c1 * (ay - bx));
-        }
-        // threads q >= 1: the partner's hi of its slot r is our slot 31 - r;
-        // thread 0 is its own partner: slot 32 - r (slot 16 for r = 0)
-        const double2 rv = shfl2(hi, partner);
-        v[E - 1 - r] = q0 ? v[E - 1 - r] : rv;
-        if (r == 0) v[E / 2] = q0 ? hi : v[E / 2];
-        else v[E - r] = q0 ? hi : v[E - r];
       }
     }
     if constexpr (KIND == K_ANALYZE) {
@@ -329,25 +346,29 @@ __global__ void __launch_bounds__(WG<M>::T, WG<M>::MINB) warp_pass(const PassArg
     if constexpr (KIND != K_SYNTH) {
     // pack: rows (j+1, j+H) from Z_k (slot r < 16) and Z_{M-k} (mirror slot:
     // slot 31 - r of the partner; thread 0: its own slot 32 - r)
+    double2 mir[E / 2];
 #pragma unroll
     for (int r = 0; r < E / 2; ++r) {
       const double2 sh = shfl2(v[E - 1 - r], partner);
-      const double2 b = q0 ? v[(E - r) & (E - 1)] : sh;
-      const int k = q + P * r;
-      const bool j0 = q0 && r == 0;
-      const double2 a = v[r];
-      double xa, xb, ya, yb;
-      if (j0) {
-        const double2 zh = v[E / 2];
-        xa = c0 * a.x; ya = c0 * a.y;
-        xb = c0 * zh.x; yb = c0 * zh.y;
-      } else {
-        xa = c1 * (a.x + b.x);
-        xb = c1 * (a.y - b.y);
-        ya = c1 * (a.y + b.y);
-        yb = c1 * (b.x - a.x);
-      }
-      if (valid) {
+      mir[r] = q0 ? v[(E - r) & (E - 1)] : sh;
+    }
+    if (valid) {
+#pragma unroll
+      for (int r = 0; r < E / 2; ++r) {
+        const int k = q + P * r;
+        const bool j0 = q0 && r == 0;
+        const double2 a = v[r], b = mir[r];
+        double xa, xb, ya, yb;
+        if (j0) {
+          const double2 zh = v[E / 2];
+          xa = c0 * a.x; ya = c0 * a.y;
+          xb = c0 * zh.x; yb = c0 * zh.y;
+        } else {
+          xa = c1 * (a.x + b.x);
+          xb = c1 * (a.y - b.y);
+          ya = c1 * (a.y + b.y);
+          yb = c1 * (b.x - a.x);
+        }
         const int64_t ia = j0 ? 0 : k + 1, ib = j0 ? 1 : k + H;
         put<false, EPI>(A, Q.bx + ia, xa, acc);
         put<false, EPI>(A, Q.bx + ib, xb, acc);
