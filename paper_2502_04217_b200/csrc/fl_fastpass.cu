@@ -82,8 +82,11 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
                        (kind != K_RESID || (reinterpret_cast<uintptr_t>(A.bhat) & 15) == 0);
   const bool group = !strided && aligned && (m == 512 || m == 2048) && A.G < (1LL << 30);
   // contiguous m = 1024: the two-stage warp-owned passes (fl_wpass.cuh, one
-  // exchange per FFT; 1024^3 gram 5.61 -> 4.74 ms).  At m = 512 they lose to
-  // the group passes (255 registers leave 8 warps per SM: 1.07 vs 0.65 ms).
+  // exchange per FFT; 1024^3 gram 5.61 -> 4.70 ms).  At m = 512 neither the
+  // 32-element form (255 registers: 8 warps per SM, 1.07 ms) nor a 16-element
+  // form with a shuffle radix-2 step (0.65 ms) beats the group passes: the
+  // fused gram there is FP64-issue bound (~150 M FP64 warp instructions, the
+  // FFT's own flop count), not exchange bound.
   const bool warp = !strided && m == 1024;
   Entry e = split ? fpk::make_split_1024(kind)
             : warp ? fpk::make_warp_1024(kind, epi)
