@@ -257,6 +257,20 @@ FL_API int fl_pcg_step_update(int64_t n, const double* sigma1, const double* sig
                               fl_stream_t stream);
 FL_API int fl_pcg_step_pupdate(int64_t n, const double* sigma1, const double* sigma2, const double* r,
                                double beta, double* p, double* out, fl_stream_t stream);
+/* Device-scalar forms for the sharded loop (no host synchronisation): the
+ * local partial is written to device memory (out_dev), alpha is read from
+ * device memory; fl_pcg_step_alpha forms curv = red2[0] + red2[1] and
+ * alpha = rho / curv (pcg.py:103-110, the host's operation order) into
+ * out_dev[0..1]; fl_fused_mask_pass_dev is fl_fused_mask_pass (gram form)
+ * with ||Z A beta||^2 written to device memory. */
+FL_API int fl_pcg_step_update_dev(int64_t n, const double* sigma1, const double* sigma2, const double* alpha_dev,
+                                  double* x, double* r, const double* p, const double* g, double* out_dev,
+                                  fl_stream_t stream);
+FL_API int fl_pcg_step_pupdate_dev(int64_t n, const double* sigma1, const double* sigma2, const double* r,
+                                   double beta, double* p, double* out_dev, fl_stream_t stream);
+FL_API int fl_pcg_step_alpha(const double* red2, const double* rho_dev, double* out_dev, fl_stream_t stream);
+FL_API int fl_fused_mask_pass_dev(fl_plan_t plan, const uint32_t* miss_bits, const double* in, double* out,
+                                  double* nrm_dev, fl_stream_t stream);
 /* Objective pieces on a full (or slab) grid given x = A beta:
  * out[0] = sum over observed (b_hat - x)^2, out[1] = sum |beta| (beta may be
  * NULL -> 0).  ipm.py:209-211. */

@@ -83,6 +83,10 @@ SIGNATURES = {
                                ctypes.POINTER(FlPcgResult), _P]),
     "fl_ipm_newton_step": (_I, [_P, _P, ctypes.POINTER(FlState), _P, _D, _D, _D, _P, _P, _P, _P, _D, _D, _I64,
                                 _P, _P]),
+    "fl_pcg_step_update_dev": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "fl_pcg_step_pupdate_dev": (_I, [_I64, _P, _P, _P, _D, _P, _P, _P]),
+    "fl_pcg_step_alpha": (_I, [_P, _P, _P, _P]),
+    "fl_fused_mask_pass_dev": (_I, [_P, _P, _P, _P, _P, _P]),
     "fl_pcg_step_init": (_I, [_I64] + [_P] * 6 + [ctypes.POINTER(_D), _P]),
     "fl_pcg_step_update": (_I, [_I64, _P, _P, _D, _P, _P, _P, _P, ctypes.POINTER(_D), _P]),
     "fl_pcg_step_pupdate": (_I, [_I64, _P, _P, _P, _D, _P, ctypes.POINTER(_D), _P]),

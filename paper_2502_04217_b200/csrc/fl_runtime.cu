@@ -247,6 +247,20 @@ int fl_fused_mask_pass(fl_plan_t p, const uint32_t* bits, const double* bhat, co
   return FL_OK;
 }
 
+int fl_fused_mask_pass_dev(fl_plan_t p, const uint32_t* bits, const double* in, double* out, double* nrm_dev,
+                           fl_stream_t stream) {
+  if (!p || !bits || !in || !out || !nrm_dev) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int last = p->ndim - 1;
+  if (p->lng[last].on) return fail(FL_E_VALUE, "norm output not available on four-step axes");
+  Scratch* sc = nullptr;
+  FL_TRY(scratch(&sc));
+  int nb = 0;
+  FL_TRY(run_pass_n(p, last, K_GRAM, in, out, bits, nullptr, nullptr, &nb, sc->partials, s));
+  const int kind = RED_SUM;
+  return finish_reduce(sc->partials, nb, 1, &kind, nrm_dev, s);
+}
+
 int fl_gram(fl_plan_t p, const uint32_t* bits, const double* beta, double* out, fl_stream_t stream) {
   if (!p || !bits || !beta || !out) return fail(FL_E_VALUE, "null argument");
   return op_gram(p, bits, nullptr, false, beta, out, nullptr, nullptr, (cudaStream_t)stream);

@@ -721,11 +721,14 @@ __global__ void k_pcg2_pupdate(int64_t n, const double* __restrict__ g1, const d
   emit(dq, SumOp(), red, partials, 0);
 }
 
+// alpha by value (host-driven sharded loop) or from device memory
+// (alpha_dev != nullptr: the device-scalar sharded loop, fl_pcg_step_alpha)
 __global__ void k_pcg2_update_a(int64_t n, const double* __restrict__ g1, const double* __restrict__ g2,
-                                double alpha, double* __restrict__ x, double* __restrict__ r,
-                                const double* __restrict__ p, const double* __restrict__ gp,
-                                double* __restrict__ partials) {
+                                double alpha_v, const double* __restrict__ alpha_dev, double* __restrict__ x,
+                                double* __restrict__ r, const double* __restrict__ p,
+                                const double* __restrict__ gp, double* __restrict__ partials) {
   __shared__ double red[32];
+  const double alpha = alpha_dev ? *alpha_dev : alpha_v;
   double rho = 0.0;
   GRID_LOOP(i, n) {
     const double pt = p[i], pb = p[n + i];
@@ -743,6 +746,15 @@ __global__ void k_pcg2_update_a(int64_t n, const double* __restrict__ g1, const 
     rho += mul(rt, P.top(rt, rb)) + mul(rb, P.bot(rt, rb));
   }
   emit(rho, SumOp(), red, partials, 0);
+}
+
+__global__ void k_step_alpha_dev(const double* __restrict__ red2, const double* __restrict__ rho,
+                                 double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    const double curv = add(red2[0], red2[1]);
+    out[0] = curv;
+    out[1] = dvd(rho[0], curv);
+  }
 }
 
 __global__ void k_objective_terms(int64_t n, const uint32_t* __restrict__ bits, const double* __restrict__ bhat,
@@ -1192,7 +1204,7 @@ int fl_pcg_step_update(int64_t n, const double* sigma1, const double* sigma2, do
   Scratch* sc;
   FL_TRY(scratch(&sc));
   const int grid = grid_for(n, T);
-  k_pcg2_update_a<<<grid, T, 0, s>>>(n, sigma1, sigma2, alpha, x, r, p, g, sc->partials);
+  k_pcg2_update_a<<<grid, T, 0, s>>>(n, sigma1, sigma2, alpha, nullptr, x, r, p, g, sc->partials);
   FL_LAUNCH_CHECK();
   const int kind = RED_SUM;
   return reduce_fetch(sc, grid, 1, &kind, out, s);
@@ -1208,6 +1220,41 @@ int fl_pcg_step_pupdate(int64_t n, const double* sigma1, const double* sigma2, c
   FL_TRY(pcg2_pupdate(n, sigma1, sigma2, r, beta, p, sc->partials, &grid, s));
   const int kind = RED_SUM;
   return reduce_fetch(sc, grid, 1, &kind, out, s);
+}
+
+int fl_pcg_step_alpha(const double* red2, const double* rho_dev, double* out_dev, fl_stream_t stream) {
+  if (!red2 || !rho_dev || !out_dev) return fail(FL_E_VALUE, "null argument");
+  k_step_alpha_dev<<<1, 32, 0, (cudaStream_t)stream>>>(red2, rho_dev, out_dev);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+// Device-scalar forms of the step-wise PCG (no host sync): the local partial
+// goes to ``out_dev`` (device), alpha comes from device memory.
+int fl_pcg_step_update_dev(int64_t n, const double* sigma1, const double* sigma2, const double* alpha_dev,
+                           double* x, double* r, const double* p, const double* g, double* out_dev,
+                           fl_stream_t stream) {
+  if (!sigma1 || !sigma2 || !alpha_dev || !x || !r || !p || !g || !out_dev) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  const int grid = grid_for(n, T);
+  k_pcg2_update_a<<<grid, T, 0, s>>>(n, sigma1, sigma2, 0.0, alpha_dev, x, r, p, g, sc->partials);
+  FL_LAUNCH_CHECK();
+  const int kind = RED_SUM;
+  return finish_reduce(sc->partials, grid, 1, &kind, out_dev, s);
+}
+
+int fl_pcg_step_pupdate_dev(int64_t n, const double* sigma1, const double* sigma2, const double* r, double beta,
+                            double* p, double* out_dev, fl_stream_t stream) {
+  if (!sigma1 || !sigma2 || !r || !p || !out_dev) return fail(FL_E_VALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch* sc;
+  FL_TRY(scratch(&sc));
+  int grid = 0;
+  FL_TRY(pcg2_pupdate(n, sigma1, sigma2, r, beta, p, sc->partials, &grid, s));
+  const int kind = RED_SUM;
+  return finish_reduce(sc->partials, grid, 1, &kind, out_dev, s);
 }
 
 int fl_objective_terms(int64_t n, const uint32_t* bits, const double* bhat, const double* x, int64_t n_beta,

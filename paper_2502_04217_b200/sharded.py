@@ -120,6 +120,11 @@ class Comm:
         """Stream-ordered cross-rank barrier (after a peer exchange)."""
         raise NotImplementedError
 
+    def reduce_device(self, tensors: list):
+        """In-place SUM of small device tensors across ranks, stream ordered,
+        no host synchronisation (one tensor per local shard)."""
+        raise NotImplementedError
+
     def peer_buffers(self, n: int):
         """Exchange buffers of ``n`` doubles: (local tensors, pointer tables),
         one per local shard; table[r] addresses rank r's buffer."""
@@ -148,6 +153,19 @@ class LocalComm(Comm):
 
     def barrier(self):
         pass  # one stream: the exchange kernels already ran in order
+
+    def reduce_device(self, tensors):
+        # NumPy's summation order over the shards (sequential below 8, the
+        # 8-way pairwise tree at 8), on the device
+        t = list(tensors)
+        if len(t) == 8:
+            acc = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]))
+        else:
+            acc = t[0].clone()
+            for x in t[1:]:
+                acc = acc + x
+        for x in t:
+            x.copy_(acc)
 
     def peer_buffers(self, n):
         bufs = [_dev.empty(n) for _ in range(self.world)]
@@ -189,6 +207,10 @@ class DistComm(Comm):
         # an all-reduce cannot complete on any rank before every rank's stream
         # reached it, i.e. before every rank's exchange kernel has finished
         t = torch.zeros(1, dtype=torch.float64, device=self.device if self.device is not None else "cpu")
+        self.dist.all_reduce(t, group=self.group)
+
+    def reduce_device(self, tensors):
+        (t,) = tensors
         self.dist.all_reduce(t, group=self.group)
 
     def peer_buffers(self, n):
@@ -324,6 +346,11 @@ class ShardOps:
         _lib.call("fl_fused_mask_pass", self.y_plan, _dev.ptr(bits), _dev.ptr(bhat) if bhat is not None else None,
                   _dev.ptr(src), _dev.ptr(dst), ctypes.byref(nrm) if want_norm else None, _dev.stream())
         return nrm.value
+
+    def fused_y_dev(self, bits, src, dst, nrm_dev):
+        """Fused gram pass with ||Z A beta||^2 (local) written to device memory."""
+        _lib.call("fl_fused_mask_pass_dev", self.y_plan, _dev.ptr(bits), _dev.ptr(src), _dev.ptr(dst),
+                  ctypes.c_void_p(nrm_dev.data_ptr()), _dev.stream())
 
     def pack_x(self, x, send):
         g = self.geo
@@ -481,12 +508,14 @@ class ShardedGrid:
         for op, y in zip(self.ops, ys):
             op.synth_y0(y, y)
 
-    def gram(self, betas, outs, bits_y, bhat_y=None, want_norm=False, extra=None):
+    def gram(self, betas, outs, bits_y, bhat_y=None, want_norm=False, extra=None, norm_dev=None):
         """outs = A^T Z A beta (bhat_y None) or A^T Z (b_hat - A beta); X-slabs in/out.
 
         Returns the all-reduced ||Z A beta||^2 when ``want_norm`` (gram only);
         with ``extra`` (one local partial per shard) the same all-reduce also
-        sums those and returns (norm, extra_sum).
+        sums those and returns (norm, extra_sum).  With ``norm_dev`` (one
+        device scalar per shard) the LOCAL norm goes there instead, with no
+        host synchronisation (the device-scalar PCG reduces it itself).
         """
         if not self._overlapped_forward(betas, outs):
             for op, b, o in zip(self.ops, betas, outs):
@@ -494,6 +523,9 @@ class ShardedGrid:
             self.x_to_y(outs, self.ybuf)
         norms = []
         for i, (op, y) in enumerate(zip(self.ops, self.ybuf)):
+            if norm_dev is not None:
+                op.fused_y_dev(bits_y[i], y, y, norm_dev[i])
+                continue
             norms.append(op.fused_y(bits_y[i], None if bhat_y is None else bhat_y[i], y, y, want_norm))
         src = self.y_to_x(self.ybuf, outs)
         for op, x, o in zip(self.ops, src, outs):
@@ -773,7 +805,19 @@ class _Work:
 
 
 def _sharded_pcg(grid: ShardedGrid, prob: ShardedProblem, ws, cfg: PcgConfig):
-    """PCG v2 over slabs (pcg.py:57-127): curvature = ||Z A p_beta||^2 + diagonal form."""
+    """PCG v2 over slabs (pcg.py:57-127): curvature = ||Z A p_beta||^2 + diagonal form.
+
+    Device scalars: the fused pass leaves the local ||Z A p||^2 on the
+    device, the two all-reduces of an iteration (curvature, r'P^{-1}r) run on
+    device buffers in stream order (``Comm.reduce_device``: NCCL between
+    GPUs), alpha = rho / curv is formed on the device (``fl_pcg_step_alpha``,
+    the host's operation order) and read by the update kernel; the host
+    synchronises ONCE per iteration, to read (curv, rho') for pcg.py's
+    breakdown checks and stopping test (it was five synchronisations: three
+    kernel partials and two all-reduces).
+    """
+    import torch
+
     comm = grid.comm
     nl = grid.geo.n_local
     L = _lib.lib()
@@ -785,43 +829,44 @@ def _sharded_pcg(grid: ShardedGrid, prob: ShardedProblem, ws, cfg: PcgConfig):
         _lib.check(L.fl_pcg_step_init(nl, _dev.ptr(w.sig1), _dev.ptr(w.sig2), _dev.ptr(w.rhs), _dev.ptr(w.x),
                                       _dev.ptr(w.r), _dev.ptr(w.p), out, s))
         parts.append([out[0], out[1]])
-    rho, dq = comm.reduce(parts, SUM)
+    rho = float(comm.reduce([[p_[0]] for p_ in parts], SUM)[0])
     if not math.isfinite(rho) or rho < 0:
         raise NumericalBreakdownError(f"preconditioner produced r'P^{{-1}}r = {rho}")
     norm = math.sqrt(rho)
     thr = cfg.abs_tol + cfg.rel_tol * norm
     if norm <= thr:
         return 0, norm
-    dq_parts = None  # local p.(K - G)p partials of the previous p-update
+    # per shard: [0] ||Z A p||^2 (local -> global), [1] p.(K-G)p (local -> global),
+    # [2] curv, [3] alpha, [4] rho, [5] rho' (local -> global)
+    slots = [torch.zeros(8, dtype=torch.float64, device=_dev.device()) for _ in ws]
+    for sl, p_ in zip(slots, parts):
+        sl[1] = p_[1]
+        sl[4] = rho
     for k in range(1, limit + 1):
-        if dq_parts is None:
-            curv_g = grid.gram([w.p[:nl] for w in ws], [w.gp for w in ws], prob.bits_y, want_norm=True)
-        else:  # one all-reduce for ||Z A p||^2 and the diagonal form
-            curv_g, dq = grid.gram([w.p[:nl] for w in ws], [w.gp for w in ws], prob.bits_y, want_norm=True,
-                                   extra=dq_parts)
-        curv = curv_g + dq
+        grid.gram([w.p[:nl] for w in ws], [w.gp for w in ws], prob.bits_y, norm_dev=[sl[0:1] for sl in slots])
+        comm.reduce_device([sl[0:2] for sl in slots])
+        for w, sl in zip(ws, slots):
+            _lib.check(L.fl_pcg_step_alpha(ctypes.c_void_p(sl.data_ptr()), ctypes.c_void_p(sl.data_ptr() + 32),
+                                           ctypes.c_void_p(sl.data_ptr() + 16), s))
+            _lib.check(L.fl_pcg_step_update_dev(nl, _dev.ptr(w.sig1), _dev.ptr(w.sig2),
+                                                ctypes.c_void_p(sl.data_ptr() + 24), _dev.ptr(w.x), _dev.ptr(w.r),
+                                                _dev.ptr(w.p), _dev.ptr(w.gp), ctypes.c_void_p(sl.data_ptr() + 40),
+                                                s))
+        comm.reduce_device([sl[5:6] for sl in slots])
+        h = slots[0][2:6].cpu().numpy()  # the iteration's one synchronisation
+        curv, rho_next = float(h[0]), float(h[3])
         if not math.isfinite(curv) or curv <= 0:
             raise NumericalBreakdownError(f"nonpositive curvature p'Kp = {curv} at iteration {k}")
-        alpha = rho / curv
-        parts = []
-        for w in ws:
-            out = ctypes.c_double()
-            _lib.check(L.fl_pcg_step_update(nl, _dev.ptr(w.sig1), _dev.ptr(w.sig2), float(alpha), _dev.ptr(w.x),
-                                            _dev.ptr(w.r), _dev.ptr(w.p), _dev.ptr(w.gp), ctypes.byref(out), s))
-            parts.append([out.value])
-        rho_next = float(comm.reduce(parts, SUM)[0])
         if not math.isfinite(rho_next) or rho_next < 0:
             raise NumericalBreakdownError(f"r'P^{{-1}}r = {rho_next} at iteration {k}")
         norm = math.sqrt(rho_next)
         if norm <= thr:
             return k, norm
         beta = rho_next / rho
-        dq_parts = []
-        for w in ws:
-            out = ctypes.c_double()
-            _lib.check(L.fl_pcg_step_pupdate(nl, _dev.ptr(w.sig1), _dev.ptr(w.sig2), _dev.ptr(w.r), float(beta),
-                                             _dev.ptr(w.p), ctypes.byref(out), s))
-            dq_parts.append(out.value)
+        for w, sl in zip(ws, slots):
+            _lib.check(L.fl_pcg_step_pupdate_dev(nl, _dev.ptr(w.sig1), _dev.ptr(w.sig2), _dev.ptr(w.r), float(beta),
+                                                 _dev.ptr(w.p), ctypes.c_void_p(sl.data_ptr() + 8), s))
+            sl[4:5].copy_(sl[5:6])
         rho = rho_next
     raise NumericalBreakdownError(f"PCG stalled at preconditioned residual {norm:.3e} after {limit} iterations")
 

@@ -47,6 +47,11 @@ def main():
         grid.synthesize_to_y(xb, y)
         err_syn = float(np.max(np.abs(y[0].numpy() - geo.y_slab(ax, r))))
         red = [comm.reduce([[float(r + 1)]], op)[0] for op in (SUM, MAX, MIN)]
+        import torch
+
+        td = torch.tensor([float(r + 1), 0.5 * (r + 1)], dtype=torch.float64)
+        comm.reduce_device([td])  # the device-scalar PCG's all-reduce (gloo: CPU tensors)
+        red += td.tolist()
         out[f"{dims} {exchange}"] = dict(gram=err_gram, norm=err_nrm, resid=err_resid, synth=err_syn, red=red)
         raw[(dims, exchange)] = (g[0].numpy().tobytes(), gr[0].numpy().tobytes(), y[0].numpy().tobytes(), nrm)
         if exchange == "peer":

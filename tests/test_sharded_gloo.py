@@ -46,7 +46,7 @@ def test_sharded_transforms_world_size_2():
         assert r["resid"] <= 1e-12, (dims, r)
         assert r["synth"] <= 1e-12, (dims, r)
         assert r["norm"] <= 1e-12, (dims, r)
-        assert r["red"] == [3.0, 2.0, 1.0]
+        assert r["red"] == [3.0, 2.0, 1.0, 3.0, 1.5]  # SUM, MAX, MIN, reduce_device SUM of [r+1, (r+1)/2]
 
 
 def test_slab_geometry_validation():
