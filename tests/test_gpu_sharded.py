@@ -279,3 +279,33 @@ def test_sharded_dropin_solve_nccl_world_size_one():
     assert rep.krylov_counts == rep1.krylov_counts
     assert abs(rep.final_objective - rep1.final_objective) <= 1e-9 * abs(rep1.final_objective)
     assert np.linalg.norm(beta - beta1) <= 1e-8 * np.linalg.norm(beta1)
+
+
+@pytest.mark.parametrize("P,dims", [(2, (128, 64, 64)), (4, (128, 128, 64))])
+def test_sharded_device_inputs_weak_scaling_shapes(P, dims):
+    """The bench's N = 2 / 4 weak-scaling grids are non-cubic ((2s, s, s),
+    (2s, 2s, s)): device-generated slab inputs and the sharded solve against
+    the single-GPU solve of the same recipe on the same grid."""
+    import torch
+
+    from paper_2502_04217_b200 import workloads
+    from paper_2502_04217_b200.masking import BraggMask, restrict
+
+    shape = fl.GridShape(dims)
+    idx, val = workloads.c4_spikes(shape.n)
+    mask = BraggMask(shape)
+    beta_t = torch.zeros(shape.n, dtype=torch.float64, device="cuda")
+    beta_t[torch.from_numpy(idx).cuda()] = torch.from_numpy(val).cuda()
+    x = fl.synthesize(beta_t, shape)
+    d0, d1, d2 = dims
+    workloads.noisy_embed_device(x, mask.on_device().bits, dims, (0, 0, 0), (d1 * d2, d2, 1), 0)
+    b = restrict(x, mask)
+    beta1, rep1 = fl.solve(b, mask, fl.IpmConfig(lam=0.5))
+    grid = sh.ShardedGrid(dims, sh.LocalComm(P), exchange="peer")
+    prob, idx2, _, lam = sh.c4_problem_device(grid, noise_seed=0)
+    betas, rep = sh.sharded_solve(prob, lam, fl.IpmConfig(lam=lam))
+    assert rep.status == rep1.status == "converged" and abs(rep.iterations - rep1.iterations) <= 1
+    assert abs(rep.final_objective - rep1.final_objective) <= 1e-9 * abs(rep1.final_objective)
+    beta = grid.geo.from_x([t.cpu().numpy() for t in betas])
+    assert np.linalg.norm(beta - beta1.cpu().numpy()) <= 1e-8 * float(beta1.norm())
+    np.testing.assert_array_equal(sh.gather_support(betas, grid.geo, grid.comm), np.sort(idx))
