@@ -7,5 +7,4 @@ timeout 600 python bench.py --emulate 8 --size 128 --steps 5 --warmup 3 > gpurun
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --sharded --size 256 --steps 5 --warmup 3 > gpurun_out/v_tr1.json 2> gpurun_out/v_tr1.err; echo "rc=$?" >> gpurun_out/v_tr1.err
 for sz in 512 1024; do
   timeout 300 python tools/pass_times.py --size $sz > gpurun_out/v_pass$sz.json 2>&1
-  FL_GPASS=0 timeout 300 python tools/pass_times.py --size $sz > gpurun_out/v_pass${sz}_old.json 2>&1
 done
