@@ -241,7 +241,7 @@ def run_b200(args, rank: int, world: int):
     op_gbps = op_bytes / (ms_per_step * 1e6)
     traffic = None
     try:  # ncu dram bytes per launch of the same kernel, committed under profiles/
-        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as fh:
+        with open(os.path.join(REPO, "profiles", "r02_traffic.json")) as fh:
             if side == 512:
                 traffic = json.load(fh)["kernels"].get(PASS_NAMES_3D[dom])
     except Exception:
