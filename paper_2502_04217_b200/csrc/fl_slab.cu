@@ -167,7 +167,8 @@ __global__ void k_y_to_x_peers(int64_t a, int64_t b, int64_t d2, int P, int me, 
 
 // Device copy of a host pointer table, cached per (device, table contents):
 // a grid's exchange tables are fixed for its lifetime, so each is uploaded
-// once (a few distinct tables per process; never freed before exit).
+// once.  Bounded: past kMaxTables distinct tables the cache is dropped after
+// a device synchronisation (no in-flight exchange can still read a table).
 int peer_table(int P, double* const* ptrs, double* const** out) {
   if (P < 1 || P > kMaxPeers) return fail(FL_E_VALUE, "peer exchange supports 1..16 ranks");
   int dev = 0;
@@ -181,6 +182,16 @@ int peer_table(int P, double* const* ptrs, double* const** out) {
   static std::map<std::vector<uintptr_t>, double**> cache;
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
+  constexpr size_t kMaxTables = 256;
+  if (it == cache.end() && cache.size() >= kMaxTables) {
+    for (auto& kv : cache) {  // each table's device: finish its work, then free
+      cudaSetDevice((int)kv.first[0]);
+      cudaDeviceSynchronize();
+      cudaFree(kv.second);
+    }
+    FL_CUDA(cudaSetDevice(dev));
+    cache.clear();
+  }
   if (it == cache.end()) {
     double** d = nullptr;
     FL_CUDA(cudaMalloc(&d, sizeof(double*) * P));
