@@ -18,7 +18,7 @@ Entry make_1024(bool strided, int kind, bool epi);
 Entry make_2048(bool strided, int kind, bool epi);
 Entry make_4096(bool strided, int kind, bool epi);
 Entry make_8192(bool strided, int kind, bool epi);
-Entry make_split_1024(int kind);
+Entry make_mirror_1024(int kind);
 Entry make_group_512(int kind, bool epi);
 Entry make_warp_1024(int kind, bool epi);
 Entry make_group_2048(int kind, bool epi);
@@ -70,11 +70,12 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
   // keyed by (device, kernel): attributes and SM counts are per device
   static std::mutex mu;
   static std::unordered_map<const void*, int> grids[kMaxDevices];
-  // strided m = 1024 synthesis / analysis: the radix-2 split into two mirrored
-  // 512-point halves (fl_split.cuh) wins on the large-stride axis (1024^3
-  // axis 0: synthesis 7.44 -> 6.36 ms, analysis 7.43 -> 6.18 ms) and loses on
-  // the 8 KiB-stride one (4.98 -> 5.94 ms), so it is chosen by stride.
-  const bool split = m == 1024 && strided && !epi && (kind == K_SYNTH || kind == K_ANALYZE) && A.inner >= 16384;
+  // strided m = 1024 synthesis / analysis: the mirrored 8 x 16 x 8 engine
+  // (fl_mirror.cuh fft1024; 512-thread CTAs, 128-byte row segments): 1024^3
+  // axis 0 6.40 / 6.19 -> 4.93 / 5.23 ms and axis 1 4.98 / 5.58 -> 4.78 / 4.87
+  // ms against the round-1 split (two mirrored 512-point halves) and E = 16
+  // engines; 256-thread CTAs (64-byte segments) were slower on both axes.
+  const bool mir = m == 1024 && strided && !epi && (kind == K_SYNTH || kind == K_ANALYZE);
   // contiguous m = 512 / 1024 / 2048: group-decoupled passes (fl_gpass.cuh);
   // they stage rows with TMA, so the row pointers must be 16-byte aligned
   // (an unaligned view falls back to the CTA-tiled engine).
@@ -88,7 +89,7 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
   // fused gram there is FP64-issue bound (~150 M FP64 warp instructions, the
   // FFT's own flop count), not exchange bound.
   const bool warp = !strided && m == 1024;
-  Entry e = split ? fpk::make_split_1024(kind)
+  Entry e = mir ? fpk::make_mirror_1024(kind)
             : warp ? fpk::make_warp_1024(kind, epi)
             : group ? (m == 512 ? fpk::make_group_512(kind, epi) : fpk::make_group_2048(kind, epi))
                     : lookup(m, strided, kind, epi);

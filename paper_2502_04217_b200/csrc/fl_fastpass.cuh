@@ -23,7 +23,6 @@
 #include "fl_common.cuh"
 #include "fl_fast.cuh"
 #include "fl_mirror.cuh"
-#include "fl_split.cuh"
 #include "fl_internal.h"
 #include "fl_passargs.cuh"
 
@@ -478,10 +477,11 @@ __global__ void __launch_bounds__(Geom<M, CFG>::T, Geom<M, CFG>::MB) fast_pass(c
 // read the mirror partner from the thread's own registers, so a pass needs only
 // the NST-1 inter-stage shared-memory exchanges.
 // ---------------------------------------------------------------------------
-template <int M, bool STRIDED, int KIND, bool EPI, int PIPE, int MB = 2>
-__global__ void __launch_bounds__(mirror::MGeom<M>::T, MB) mirror_pass(const PassArgs A) {
-  using G = mirror::MGeom<M>;
-  constexpr int CFG = cfg_code(0, PIPE, 2, 1);  // staging geometry shared with Geom<M, CFG>
+template <int M, bool STRIDED, int KIND, bool EPI, int PIPE, int MB = 2, int TT = 0>
+__global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const PassArgs A) {
+  using G = mirror::MGeom<M, TT>;
+  // staging geometry shared with Geom<M, CFG> (512-thread CTAs: T_SEL 1)
+  constexpr int CFG = G::T == 512 ? cfg_code(1, PIPE, 1, 1) : cfg_code(0, PIPE, 2, 1);
   static_assert(Geom<M, CFG>::P == G::P && Geom<M, CFG>::W == G::W, "staging geometry mismatch");
   static_assert(Geom<M, CFG>::PIPE == PIPE, "staging does not fit");
   constexpr int P = G::P, W = G::W, H = G::H;
@@ -706,8 +706,9 @@ struct Entry {
 //   * everything else at m <= 512: 256-thread CTAs with single-buffer
 //     staging; m >= 1024: the same with one CTA per SM and the full register
 //     budget (E = 16);
-//   * contiguous m = 512 / 1024 / 2048 passes and strided m = 1024 at large
-//     stride are dispatched before this table (fl_gpass.cuh, fl_split.cuh).
+//   * contiguous m = 512 / 1024 / 2048 passes and every strided m = 1024
+//     stride are dispatched before this table (fl_gpass.cuh, fl_wpass.cuh,
+//     fl_mirror.cuh fft1024).
 constexpr int kCfgLight = cfg_code(1, 0, 2);
 constexpr int kCfgHeavy = cfg_code(0, 1, 2);
 constexpr int kCfgLong = cfg_code(0, 1, 1);
@@ -764,8 +765,23 @@ Entry make(int kind, bool epi) {
                                                        : fast_pass<M, S, K_ANALYZE, false, kCfgLight>);
     }
   }
-  if constexpr (M >= 1024) return make_heavy<M, S, kCfgLong>(kind, epi);
+  if constexpr (M == 1024 && S) return Entry();  // dispatched to the mirrored engine (make_mirror1024)
+  else if constexpr (M >= 1024) return make_heavy<M, S, kCfgLong>(kind, epi);
   else return make_heavy<M, S, kCfgHeavy>(kind, epi);
+}
+
+// strided m = 1024 synthesis / analysis on the mirrored 8 x 16 x 8 engine
+// (512-thread CTAs: 8 fibre pairs = 128-byte row segments, one CTA per SM)
+template <int M = 1024>  // a template: instantiated only in the TU that uses it
+Entry make_mirror1024(int kind) {
+  using G = mirror::MGeom<M>;
+  Entry e;
+  e.fn = kind == K_SYNTH ? mirror_pass<M, true, K_SYNTH, false, 0, 1>
+                         : mirror_pass<M, true, K_ANALYZE, false, 0, 1>;
+  e.threads = G::T;
+  e.smem = G::FIB_BYTES;
+  e.w = G::W;
+  return e;
 }
 
 template <int M>

@@ -15,16 +15,8 @@ Entry make_8192(bool strided, int kind, bool epi) { return make_any<8192>(stride
 Entry make_warp_1024(int kind, bool epi) { return wpk::make_warp<1024>(kind, epi); }
 Entry make_group_2048(int kind, bool epi) { return gpk::make_group<2048>(kind, epi); }
 
-// strided m = 1024 as two mirrored 512-point halves (fl_split.cuh)
-Entry make_split_1024(int kind) {
-  Entry e;
-  if (kind == K_SYNTH) e.fn = split::split_pass<K_SYNTH>;
-  else if (kind == K_ANALYZE) e.fn = split::split_pass<K_ANALYZE>;
-  e.threads = split::T;
-  e.smem = split::SMEM;
-  e.w = split::W;
-  return e;
-}
+// strided m = 1024: the mirrored 8 x 16 x 8 engine (fl_mirror.cuh)
+Entry make_mirror_1024(int kind) { return make_mirror1024<1024>(kind); }
 
 }  // namespace fpk
 }  // namespace fl

@@ -26,12 +26,14 @@ using fast::si;
 
 constexpr int log8(int m) { return m <= 1 ? 0 : 1 + log8(m / 8); }
 
-template <int M>
+template <int M, int TT = 0>
 struct MGeom {
   static constexpr int E = 16;
   static constexpr int NB = M / 8;                          // butterflies per fibre per stage
   static constexpr int P = NB / 2;                          // threads per fibre
-  static constexpr int T = fast::imax(256, P);              // threads per CTA
+  // threads per CTA: 256 (two CTAs per SM); m = 1024 (64 threads per pair):
+  // 512, so a tile is still 8 fibre pairs = 128-byte row segments; TT forces T
+  static constexpr int T = TT ? TT : (M == 1024 ? 512 : fast::imax(256, P));
   static constexpr int W = T / P;                           // fibres per CTA tile
   static constexpr int NST = log8(M);
   static constexpr int FS = M + M / 8 + 1;                  // smem fibre stride (double2)
@@ -94,12 +96,78 @@ __device__ __forceinline__ void exchange(double2* v, double2* fib, int q) {
   __syncthreads();
 }
 
+// m = 1024 = 8 x 16 x 8: Stockham stages of radix 8 (spans 1), 16 (span 8) and
+// 8 (span 128).  The first and last stages have 128 butterflies and keep the
+// mirror ownership {q, 128 - q} (so unpack and pack find Z_k and Z_{m-k} in
+// the same thread, exactly as for 8^k); the middle radix-16 stage has one
+// butterfly per thread (butterfly q: positions q + 64 t).
+__device__ __forceinline__ void fft1024(double2* v, double2* fib, int q, const double2* tw, int sign) {
+  constexpr int NB = 128;
+  const int o0 = own(q, 0, NB), o1 = own(q, 1, NB);
+  dft8(v, sign);
+  dft8(v + 8, sign);
+  {  // stage 0 (span 1): outputs at 8 qq + t, si = 9 qq + t
+    double2* a = fib + 9 * o0;
+    double2* b = fib + 9 * o1;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      a[t] = v[t];
+      b[t] = v[8 + t];
+    }
+  }
+  __syncthreads();
+  {  // stage 1 inputs: q + 64 t, si = si(q) + 72 t
+    const double2* a = fib + si(q);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = a[72 * t];
+  }
+  __syncthreads();
+  const int j = q & 7;  // span 8: twiddle w128^(j t)
+  if (j) {
+    double2 w[16];
+    fast::twiddles<1024, 16, 8>(w, j, tw, sign);
+#pragma unroll
+    for (int t = 1; t < 16; ++t) v[t] = cmul(v[t], w[t]);
+  }
+  fast::dft_gather<16, 1>(v, sign);
+  {  // stage 1 outputs: (q - j) 16 + j + 8 t, si = si(base) + 9 t
+    double2* a = fib + si((q - j) * 16 + j);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) a[9 * t] = v[t];
+  }
+  __syncthreads();
+  {  // stage 2 inputs: own + 128 t, si = si(own) + 144 t
+    const double2* a = fib + si(o0);
+    const double2* b = fib + si(o1);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      v[t] = a[144 * t];
+      v[8 + t] = b[144 * t];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {  // stage 2 (span 128): twiddle w1024^(own t), outputs own + 128 t
+    const int ob = b ? o1 : o0;
+    double2 w[8];
+    fast::twiddles<1024, 8, 128>(w, ob, tw, sign);
+#pragma unroll
+    for (int t = 1; t < 8; ++t) v[8 * b + t] = cmul(v[8 * b + t], w[t]);
+    dft8(v + 8 * b, sign);
+  }
+}
+
 template <int M, int S = 0, int TM = M>
 __device__ __forceinline__ void fft(double2* v, double2* fib, int q, const double2* tw, int sign) {
+  if constexpr (M == 1024) {
+    fft1024(v, fib, q, tw, sign);
+    return;
+  } else {
   stage<M, S, TM>(v, q, tw, sign);
   if constexpr (S + 1 < MGeom<M>::NST) {
     exchange<M, S>(v, fib, q);
     fft<M, S + 1, TM>(v, fib, q, tw, sign);
+  }
   }
 }
 

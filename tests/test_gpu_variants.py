@@ -6,8 +6,8 @@ families are reached through the grid shape: the mirrored engine (strided
 m = 64 / 512 / 4096), the E = 8 engine (other strided lengths <= 256, all
 contiguous lengths outside the group set), the group-decoupled contiguous
 passes (m = 512 / 2048, fl_gpass.cuh), the two-stage warp passes (contiguous
-m = 1024, fl_wpass.cuh), the long-fibre E = 16 engine
-and the radix-2 split (strided m = 1024, chosen by stride), the generic
+m = 1024, fl_wpass.cuh), the mirrored 8 x 16 x 8 engine (strided m = 1024),
+the long-fibre E = 16 engine (longer strided fibres), the generic
 mixed-radix engine (non-power-of-two even lengths) and the four-step path
 (lengths above 8192).
 """
@@ -29,8 +29,8 @@ DIMS = [
     # mirrored m = 64 / 4096 strided, E = 8 lengths, group m = 1024 / 2048 contiguous
     (64, 8, 16), (8, 4096), (4096, 4), (64, 64, 64), (256, 32, 256), (32, 128, 128),
     (4, 1024), (6, 2048), (2, 8, 1024),
-    # strided m = 1024: E = 16 engine (small stride) and radix-2 split (stride >= 16384)
-    (1024, 8, 16), (8, 1024, 24), (1024, 1024), (1024, 4, 4096),
+    # strided m = 1024 (mirrored 8 x 16 x 8) at small and large strides; strided 2048 (E = 16)
+    (1024, 8, 16), (8, 1024, 24), (1024, 1024), (1024, 4, 4096), (2048, 4, 8),
     # generic mixed-radix and four-step
     (24, 36), (6, 10, 4), (96, 40, 24), (16384,), (2, 16384),
 ]

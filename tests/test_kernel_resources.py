@@ -22,8 +22,7 @@ HOT = [
     r"mirror_passILi512ELb1ELi[01]ELb0",   # strided m = 512 synthesis / analysis
     r"group_passILi512ELi[012]E",          # contiguous m = 512: synth, analysis, fused gram
     r"warp_passILi1024ELi[012]E",          # contiguous m = 1024 (C5 axes): synth, analysis, fused gram
-    r"split_pass",                         # strided m = 1024, large stride
-    r"fast_passILi1024ELb1ELi[01]ELb0",    # strided m = 1024, small stride (E = 16)
+    r"mirror_passILi1024ELb1ELi[01]ELb0",  # strided m = 1024 (mirrored 8 x 16 x 8 engine)
     r"k_kkt_epilogue", r"k_pcg2", r"k_newton_setup", r"k_update", r"k_assess", r"k_ratios",
 ]
 # known spills, all off the BASELINE hot path: small strided lengths on
