@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2502_04217_b200 as fl  # noqa: E402
-from paper_2502_04217_b200 import _lib, newton_system, workloads  # noqa: E402
+from paper_2502_04217_b200 import _lib, ipm, newton_system, workloads  # noqa: E402
 
 
 def _events(fn, reps):
@@ -67,7 +67,7 @@ def main():
                     "record_wall_us": [round(r.wall_time * 1e6, 1) for r in rep.records]}
     _lib.call("fl_set_pcg_loop", 3)
     n = mask.shape.n
-    st = fl.initial_state(b, mask, inst.lam)
+    st = ipm.initial_state(b, mask, inst.lam)
     diag = newton_system.barrier_diagonals(st.s1, st.s2, st.nu1, st.nu2)
     db = torch.randn(n, dtype=torch.float64, device="cuda")
     dz = torch.randn(n, dtype=torch.float64, device="cuda")
