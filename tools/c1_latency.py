@@ -44,6 +44,7 @@ def _wall(fn, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--host-profile", action="store_true")
     a = ap.parse_args()
     inst = workloads.c1_1d(seed=0)
     mask = fl.Mask.from_bool(inst.flags, fl.GridShape(inst.dims))
@@ -78,5 +79,29 @@ def main():
     print(json.dumps(out), flush=True)
 
 
+
+
+def host_profile(reps=50):
+    """cProfile of `reps` C1 solves (host-side cost per IPM iteration)."""
+    import cProfile
+    import pstats
+
+    inst = workloads.c1_1d(seed=0)
+    mask = fl.Mask.from_bool(inst.flags, fl.GridShape(inst.dims))
+    b = fl.observe(torch.from_numpy(inst.beta_true).cuda(), mask)
+    b += torch.from_numpy(inst.noise).cuda()
+    cfg = fl.IpmConfig(lam=inst.lam)
+    fl.solve(b, mask, cfg)
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(reps):
+        fl.solve(b, mask, cfg)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(40)
+
+
 if __name__ == "__main__":
-    main()
+    if "--host-profile" in sys.argv:
+        host_profile()
+    else:
+        main()
