@@ -44,21 +44,32 @@ METRIC = "KKT matvecs/s at 512^3 (condensed K apply, C4 Bragg-punched grid)"
 UNIT = "matvec/s"
 PASS_NAMES_3D = ["synth_axis0", "synth_axis1", "gram_mid_axis2", "analyze_axis1", "analyze_axis0",
                  "kkt_epilogue"]
+# operator order B (fl_kkt_order 1: 3D with axes 0 and 2 of 512): contiguous axis
+# first and last, the fused mask pass on axis 0, the epilogue fused into the last pass
+PASS_NAMES_3D_B = ["synth_axis2", "synth_axis1", "gram_mask_axis0", "analyze_axis1",
+                   "analyze_axis2_kkt_epilogue"]
 
 
-def alg_bytes_per_pass(n: int, ndim: int) -> list[float]:
-    """Minimum HBM bytes of each launch of one KKT matvec as executed.
+def pass_layout(plan_handle, n: int, ndim: int):
+    """(names, minimum HBM bytes) of each launch of one KKT matvec as executed.
 
-    2d-1 transform passes (read + write one fp64 grid; the fused mask pass
-    also reads the n/8-byte bitmask) and the elementwise epilogue (reads g,
-    d_beta, d_z, sigma1, sigma2; writes top, bottom).  The operator-level
-    algorithmic model of SURVEY 8d (120.125 B/voxel) counts the epilogue as
-    fused into the last transform pass; executed traffic is 136.125 B/voxel.
+    Transform passes read + write one fp64 grid (16 B/voxel; the fused mask
+    pass also reads the n/8-byte bitmask); the KKT epilogue reads d_beta, d_z,
+    sigma1, sigma2 and writes top, bottom.  Order A runs it as a separate pass
+    that also reads g (56 B/voxel; 136.125 executed B/voxel per matvec); order B
+    fuses it into the last analysis (16 + 40 = 56 B/voxel for that pass), which
+    executes exactly the 120.125 B/voxel operator model of SURVEY 8d.
     """
+    from paper_2502_04217_b200 import _lib
+
     if ndim == 1:
-        return [16.125 * n, 56.0 * n]
+        return ["gram_mask_axis0", "kkt_epilogue"], [16.125 * n, 56.0 * n]
     mid = 16.0 * n + n / 8.0
-    return [16.0 * n] * (ndim - 1) + [mid] + [16.0 * n] * (ndim - 1) + [56.0 * n]
+    if ndim == 3 and _lib.lib().fl_kkt_order(plan_handle) == 1:
+        return PASS_NAMES_3D_B, [16.0 * n, 16.0 * n, mid, 16.0 * n, 56.0 * n]
+    names = ([f"synth_axis{a}" for a in range(ndim - 1)] + [f"gram_mid_axis{ndim - 1}"]
+             + [f"analyze_axis{a}" for a in range(ndim - 2, -1, -1)] + ["kkt_epilogue"])
+    return names, [16.0 * n] * (ndim - 1) + [mid] + [16.0 * n] * (ndim - 1) + [56.0 * n]
 
 
 def bench_config(size: int, world: int) -> dict:
@@ -220,7 +231,8 @@ def run_b200(args, rank: int, world: int):
     value = world * args.steps / (ms_max / 1e3)
 
     # per-pass split (live CUDA events between passes)
-    npass = 2 * len(dims)
+    names, alg = pass_layout(plan.handle, n, len(dims))
+    npass = len(names)
     acc = np.zeros(npass)
     reps = max(3, min(10, args.steps))
     buf = (__import__("ctypes").c_double * 8)()
@@ -232,8 +244,7 @@ def run_b200(args, rank: int, world: int):
         acc += np.array(buf[:npass])
     pass_ms = acc / reps
     peak, peak_src = measured_peak_hbm()
-    alg = alg_bytes_per_pass(n, len(dims))
-    passes = [{"name": PASS_NAMES_3D[i], "ms": round(float(pass_ms[i]), 4),
+    passes = [{"name": names[i], "ms": round(float(pass_ms[i]), 4),
                "alg_bytes": alg[i], "GBps": round(alg[i] / pass_ms[i] / 1e6, 1),
                "frac": round(alg[i] / pass_ms[i] / 1e6 / peak, 4)} for i in range(npass)]
     dom = int(np.argmax(pass_ms))
@@ -243,10 +254,10 @@ def run_b200(args, rank: int, world: int):
     try:  # ncu dram bytes per launch of the same kernel, committed under profiles/
         with open(os.path.join(REPO, "profiles", "r02_traffic.json")) as fh:
             if side == 512:
-                traffic = json.load(fh)["kernels"].get(PASS_NAMES_3D[dom])
+                traffic = json.load(fh)["kernels"].get(names[dom])
     except Exception:
         traffic = None
-    roofline = {"bound": "hbm", "kernel": PASS_NAMES_3D[dom], "achieved": round(alg[dom] / pass_ms[dom] / 1e6, 1),
+    roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(alg[dom] / pass_ms[dom] / 1e6, 1),
                 "peak": peak, "unit": "GB/s", "frac": round(alg[dom] / pass_ms[dom] / 1e6 / peak, 4),
                 "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_launch": alg[dom]}
@@ -337,23 +348,23 @@ def per_pass_table(side: int, reps: int = 5):
     top, bot = _dev.empty(n), _dev.empty(n)
     buf = (ctypes.c_double * 8)()
     cnt = ctypes.c_int()
-    acc = np.zeros(6)
+    names, alg = pass_layout(plan.handle, n, 3)
+    acc = np.zeros(len(names))
     for i in range(reps + 2):
         _lib.call("fl_kkt_apply_profiled", plan.handle, _dev.ptr(dm.bits), _dev.ptr(sig1), _dev.ptr(sig2),
                   _dev.ptr(d[:n]), _dev.ptr(d[n:]), _dev.ptr(top), _dev.ptr(bot), buf, ctypes.byref(cnt),
                   _dev.stream())
         if i >= 2:
-            acc += np.array(buf[:6])
+            acc += np.array(buf[:len(names)])
     ms = acc / reps
     peak, _ = measured_peak_hbm()
-    alg = alg_bytes_per_pass(n, 3)
     del sig1, sig2, d, top, bot, dm
     torch.cuda.empty_cache()
     return {"size": side, "matvec_ms": round(float(ms.sum()), 3), "matvec_per_s": round(1e3 / float(ms.sum()), 2),
             "operator_frac": round(120.125 * n / (float(ms.sum()) * 1e6) / peak, 4),
-            "passes": [{"name": PASS_NAMES_3D[i], "ms": round(float(ms[i]), 4),
+            "passes": [{"name": names[i], "ms": round(float(ms[i]), 4),
                         "GBps": round(alg[i] / ms[i] / 1e6, 1), "frac": round(alg[i] / ms[i] / 1e6 / peak, 4)}
-                       for i in range(6)]}
+                       for i in range(len(names))]}
 
 
 def weak_dims(world: int, side: int = 512):

@@ -192,9 +192,16 @@ FL_API int fl_kkt_apply(fl_plan_t plan, const uint32_t* miss_bits, const double*
                  const double* sigma2, const double* d_beta, const double* d_z, double* top,
                  double* bottom, double* pkp_host, fl_stream_t stream);
 /* fl_kkt_apply with a cudaEvent after every HBM pass; writes the per-pass
- * device times (ms) to ``pass_ms`` (host, 2*ndim entries: 2*ndim-1 transform
- * passes + the elementwise KKT epilogue) and returns the
- * number of passes in ``npasses``.  Measurement hook for bench.py. */
+ * device times (ms) to ``pass_ms`` (host, up to 2*ndim entries) and the
+ * number of passes to ``npasses``: order A (fl_kkt_order 0) 2*ndim-1
+ * transform passes + the elementwise KKT epilogue; order B (1) 2*ndim-1
+ * transform passes, the epilogue fused into the last.  Measurement hook for
+ * bench.py. */
+/* Operator order of fl_kkt_apply for this plan: 0 = axis-0 synthesis first,
+ * fused mask pass on the contiguous axis, separate KKT epilogue; 1 = the
+ * contiguous axis first and last (fused mask pass on axis 0, epilogue fused
+ * into the final contiguous analysis; 3D grids with axes 0 and 2 of 512). */
+FL_API int fl_kkt_order(fl_plan_t plan);
 FL_API int fl_kkt_apply_profiled(fl_plan_t plan, const uint32_t* miss_bits, const double* sigma1,
                                  const double* sigma2, const double* d_beta, const double* d_z,
                                  double* top, double* bottom, double* pass_ms, int* npasses,

@@ -72,6 +72,7 @@ SIGNATURES = {
     "fl_barrier_diagonals": (_I, [_I64] + [_P] * 10 + [_P]),
     "fl_kkt_apply": (_I, [_P] * 8 + [ctypes.POINTER(_D), _P]),
     "fl_kkt_epilogue": (_I, [_I64] + [_P] * 6 + [ctypes.POINTER(_D), _P]),
+    "fl_kkt_order": (_I, [_P]),
     "fl_kkt_apply_profiled": (_I, [_P] * 8 + [ctypes.POINTER(_D), ctypes.POINTER(_I), _P]),
     "fl_precond_apply": (_I, [_I64] + [_P] * 6 + [_P]),
     "fl_newton_rhs": (_I, [_I64, ctypes.POINTER(FlState), _P, _P, _P, _D, _D] + [_P] * 8 + [_P]),

@@ -500,11 +500,24 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
     if ((int64_t)blockIdx.x < ntiles) issue_tile<M, STRIDED, CFG>(A, blockIdx.x, stage0, c, q);
     cp_commit();
   }
+  // strided fused mask pass: when a tile's 8 pairs (16 voxels) share one mask
+  // word per row k (row stride a multiple of 32 voxels), the tile's M words are
+  // staged in shared memory by the whole CTA (2 words per thread) instead of 16
+  // word loads per thread held in registers across the inverse FFT
+  // (run_pass_n sends strided fused passes only with A.inner % 32 == 0)
+  constexpr bool SMASK = STRIDED && KIND == K_GRAM;
+  uint32_t* mw = reinterpret_cast<uint32_t*>(smem + G::FIB_BYTES / 16);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t g = tile * W + c;
     const bool valid = g < A.G;
     const Geo Q = geo<STRIDED>(A, valid ? g : 0);
     const int64_t next = tile + gridDim.x;
+    if constexpr (SMASK) {  // the previous tile's reads ended at its forward FFT's first barrier
+      const Geo Q0 = geo<STRIDED>(A, tile * W);
+      const uint32_t* wb = A.bits + (Q0.bx >> 5);
+      const int64_t wst = Q0.st >> 5;
+      for (int k = threadIdx.x; k < M; k += G::T) mw[k] = __ldg(wb + k * wst);
+    }
     if (PIPE > 0) {
       cp_wait<0>();
       __syncthreads();
@@ -574,7 +587,7 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
         mbits |= ((wx >> (t & 31)) & 1u) << (2 * i);
         mbits |= ((wy >> (t & 31)) & 1u) << (2 * i + 1);
       }
-    } else if constexpr (KIND == K_GRAM || KIND == K_RESID) {
+    } else if constexpr ((KIND == K_GRAM || KIND == K_RESID) && !SMASK) {
       if (valid) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -619,12 +632,19 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
             if (valid) {
               const int64_t t = mirror::slot_k<M>(q, b, s);
               const int64_t vx = Q.bx + t * Q.st;
-              const bool mx = (mbits >> (2 * (8 * b + s))) & 1u;
+              bool mx, my;
+              if constexpr (SMASK) {  // x and y bits of this pair in the tile row's word
+                const uint32_t w = mw[t] >> (Q.bx & 31);
+                mx = w & 1u;
+                my = (w >> 1) & 1u;
+              } else {
+                mx = (mbits >> (2 * (8 * b + s))) & 1u;
+                my = (mbits >> (2 * (8 * b + s) + 1)) & 1u;
+              }
               if (KIND == K_RESID) z.x = mx ? 0.0 : A.bhat[vx] - z.x;
               else if (mx) z.x = 0.0;
               if (Q.by >= 0) {
                 const int64_t vy = Q.by + t * Q.st;
-                const bool my = (mbits >> (2 * (8 * b + s) + 1)) & 1u;
                 if (KIND == K_RESID) z.y = my ? 0.0 : A.bhat[vy] - z.y;
                 else if (my) z.y = 0.0;
               } else {
@@ -755,6 +775,20 @@ Entry make(int kind, bool epi) {
       e.fn = kind == K_SYNTH ? mirror_pass<M, true, K_SYNTH, false, 0> : mirror_pass<M, true, K_ANALYZE, false, 0>;
       e.threads = G::T;
       e.smem = G::FIB_BYTES;
+      e.w = G::W;
+      return e;
+    }
+  }
+  if constexpr (S && M == 512) {
+    // strided fused gram: the mask pass of the axis-0-last operator order
+    // (op_gram, KKT apply at 512^3) on the mirrored engine, the tile's mask
+    // words staged in shared memory
+    if (kind == K_GRAM && !epi) {
+      using G = mirror::MGeom<M>;
+      Entry e;
+      e.fn = mirror_pass<M, true, K_GRAM, false, 0>;
+      e.threads = G::T;
+      e.smem = G::FIB_BYTES + M * 4;
       e.w = G::W;
       return e;
     }

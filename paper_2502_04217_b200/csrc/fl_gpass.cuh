@@ -130,6 +130,17 @@ __global__ void __launch_bounds__(GCfg<M>::T, GCfg<M>::MINB) group_pass(const Pa
     auto refill_next = [&]() {
       if (leader && gn < npairs) tma_rows<M>(A.in, geo<false>(A, gn), stage, bar);
     };
+    if constexpr (EPI) {
+      // the KKT epilogue's operand rows of this pair (read after the FFT): into L2 now
+      if (leader) {
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          const double* src = o == 0 ? A.epi.pb : o == 1 ? A.epi.pz : o == 2 ? A.epi.sig1 : A.epi.sig2;
+          fast::bulk_prefetch_l2(src + Q.bx, M * 8u);
+          if (has_y) fast::bulk_prefetch_l2(src + Q.by, M * 8u);
+        }
+      }
+    }
     fast::mbar_wait(bar, ph0);
     ph0 ^= 1u;
     double2 v[E];

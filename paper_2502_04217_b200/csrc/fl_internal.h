@@ -68,6 +68,9 @@ int op_analyze(const fl_plan* p, const double* in, double* out, cudaStream_t s);
 int op_gram(const fl_plan* p, const uint32_t* bits, const double* bhat, bool resid,
             const double* in, double* out, const KktEpi* epi, int* nblocks, cudaStream_t s);
 
+// KKT apply in the axis-0-last order with the epilogue fused (fl_pass.cu)
+bool kkt_order_b(const fl_plan* p);
+
 // Elementwise KKT epilogue on a gram output (fl_vec.cu); n even.
 int kkt_epilogue(int64_t n, double* g, const double* pb, const double* pz, const double* sig1,
                  const double* sig2, double* bottom, double* partials, int* nblocks, cudaStream_t s);

@@ -322,6 +322,8 @@ int fl_kkt_epilogue(int64_t n, double* g, const double* d_beta, const double* d_
   return FL_OK;
 }
 
+int fl_kkt_order(fl_plan_t p) { return p && kkt_order_b(p) ? 1 : 0; }
+
 int fl_kkt_apply_profiled(fl_plan_t p, const uint32_t* bits, const double* sigma1,
                           const double* sigma2, const double* d_beta, const double* d_z, double* top,
                           double* bottom, double* pass_ms, int* npasses, fl_stream_t stream) {
@@ -329,13 +331,32 @@ int fl_kkt_apply_profiled(fl_plan_t p, const uint32_t* bits, const double* sigma
     return fail(FL_E_VALUE, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   const int d = p->ndim;
-  const int np = 2 * d;  // 2d-1 transform passes + the elementwise epilogue
+  const int np = 2 * d;  // at most 2d-1 transform passes + the elementwise epilogue
   cudaEvent_t ev[8];
   for (int i = 0; i <= np; ++i) FL_CUDA(cudaEventCreate(&ev[i]));
   int st = FL_OK;
   FL_CUDA(cudaEventRecord(ev[0], s));
   int k = 0;
-  if (d == 1) {
+  if (kkt_order_b(p)) {  // same order as fl_kkt_apply (op_gram)
+    const double* src = d_beta;
+    for (int a = d - 1; a >= 1 && st == FL_OK; --a) {
+      st = run_pass(p, a, K_SYNTH, src, top, nullptr, nullptr, nullptr, nullptr, s);
+      cudaEventRecord(ev[++k], s);
+      src = top;
+    }
+    if (st == FL_OK) st = run_pass(p, 0, K_GRAM, top, top, bits, nullptr, nullptr, nullptr, s);
+    cudaEventRecord(ev[++k], s);
+    KktEpi e;
+    e.pb = d_beta;
+    e.pz = d_z;
+    e.sig1 = sigma1;
+    e.sig2 = sigma2;
+    e.bottom = bottom;
+    for (int a = 1; a < d && st == FL_OK; ++a) {
+      st = run_pass(p, a, K_ANALYZE, top, top, nullptr, nullptr, a == d - 1 ? &e : nullptr, nullptr, s);
+      cudaEventRecord(ev[++k], s);
+    }
+  } else if (d == 1) {
     st = run_pass(p, 0, K_GRAM, d_beta, top, bits, nullptr, nullptr, nullptr, s);
     cudaEventRecord(ev[++k], s);
   } else {
@@ -352,16 +373,18 @@ int fl_kkt_apply_profiled(fl_plan_t p, const uint32_t* bits, const double* sigma
       cudaEventRecord(ev[++k], s);
     }
   }
-  if (st == FL_OK) st = kkt_epilogue(p->n, top, d_beta, d_z, sigma1, sigma2, bottom, nullptr, nullptr, s);
-  cudaEventRecord(ev[++k], s);
+  if (!kkt_order_b(p)) {
+    if (st == FL_OK) st = kkt_epilogue(p->n, top, d_beta, d_z, sigma1, sigma2, bottom, nullptr, nullptr, s);
+    cudaEventRecord(ev[++k], s);
+  }
   if (st == FL_OK) {
-    FL_CUDA(cudaEventSynchronize(ev[np]));
-    for (int i = 0; i < np; ++i) {
+    FL_CUDA(cudaEventSynchronize(ev[k]));
+    for (int i = 0; i < k; ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
       pass_ms[i] = ms;
     }
-    *npasses = np;
+    *npasses = k;
   }
   for (int i = 0; i <= np; ++i) cudaEventDestroy(ev[i]);
   return st;

@@ -266,9 +266,9 @@ class Problem:
                   ctypes.byref(out), _dev.stream())
         return out.value
 
-    def assess(self, st: IpmState, g, lam: float, mu: float) -> _lib.FlAssess:
+    def assess(self, st: IpmState, g, lam: float, mu: float, fs=None) -> _lib.FlAssess:
         a = _lib.FlAssess()
-        fs = fl_state(st)
+        fs = fl_state(st) if fs is None else fs
         _lib.call("fl_ipm_assess", self.n, ctypes.byref(fs), _dev.ptr(g), float(lam), float(mu),
                   ctypes.byref(a), _dev.stream())
         return a
@@ -558,7 +558,7 @@ def solve(b, mask: Mask, config: IpmConfig = IpmConfig(),
     best_kkt = math.inf
     status = "max_iters"
     prob.residual_adjoint(st.beta, ws.g)
-    a = prob.assess(st, ws.g, lam, st.mu)
+    a = prob.assess(st, ws.g, lam, st.mu, ws.fs)
     conv = _conv_report(a, n, config.tol, config.gamma_centrality)
 
     for iteration in range(1, config.max_iters + 1):
@@ -572,12 +572,12 @@ def solve(b, mask: Mask, config: IpmConfig = IpmConfig(),
         if _ASYNC_STEP:
             _launch_step(prob, ws, st.mu, lam, config)
             prob.residual_adjoint(st.beta, ws.g)
-            a = prob.assess(st, ws.g, lam, st.mu)
+            a = prob.assess(st, ws.g, lam, st.mu, ws.fs)
             res, alpha_p, alpha_d = _step_verdict(ws)
         else:
             res, alpha_p, alpha_d = _fused_step(prob, ws, st.mu, lam, config)
             prob.residual_adjoint(st.beta, ws.g)
-            a = prob.assess(st, ws.g, lam, st.mu)
+            a = prob.assess(st, ws.g, lam, st.mu, ws.fs)
         conv = _conv_report(a, n, config.tol, config.gamma_centrality)
         record = IterationRecord(
             iteration=iteration,

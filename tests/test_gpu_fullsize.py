@@ -99,3 +99,33 @@ def test_sharded_gram_c5_layout_matches_single_gpu(grid):
     got = torch.cat(out)
     del out, xs
     assert _rel_max(got, ref) <= 1e-12
+
+
+def test_kkt_apply_operator_order(grid):
+    """fl_kkt_apply's operator order (fl_kkt_order): at 512^3 order B (the
+    contiguous axis first and last, the fused mask pass on axis 0, the KKT
+    epilogue fused into the final analysis), at 1024^3 order A.  Either way
+    the result equals the gram (order A, fl_gram) followed by the separate
+    epilogue pass: top to rounding, bottom bitwise (it does not depend on the
+    gram), d.Kd to rounding."""
+    import ctypes
+
+    from paper_2502_04217_b200 import _dev, _lib
+
+    side, shape, mask = grid
+    n = shape.n
+    plan = _dev.plan_for(shape.dims)
+    assert _lib.lib().fl_kkt_order(plan.handle) == (1 if side == 512 else 0)
+    s1, s2 = _rand(n, 30).abs() + 0.4, _rand(n, 31).abs() + 0.4
+    db, dz = _rand(n, 32), _rand(n, 33)
+    bits = mask.on_device().bits
+    top, bot, pkp = _dev.empty(n), _dev.empty(n), ctypes.c_double()
+    _lib.call("fl_kkt_apply", plan.handle, _dev.ptr(bits), _dev.ptr(s1), _dev.ptr(s2), _dev.ptr(db),
+              _dev.ptr(dz), _dev.ptr(top), _dev.ptr(bot), ctypes.byref(pkp), _dev.stream())
+    g = fl.gram(db, mask)
+    bot2, pkp2 = _dev.empty(n), ctypes.c_double()
+    _lib.call("fl_kkt_epilogue", n, _dev.ptr(g), _dev.ptr(db), _dev.ptr(dz), _dev.ptr(s1), _dev.ptr(s2),
+              _dev.ptr(bot2), ctypes.byref(pkp2), _dev.stream())
+    assert _rel_max(top, g) <= 1e-12
+    assert torch.equal(bot, bot2)
+    assert abs(pkp.value - pkp2.value) <= 1e-12 * abs(pkp2.value)

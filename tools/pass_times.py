@@ -20,9 +20,6 @@ import torch  # noqa: E402
 import paper_2502_04217_b200 as fl  # noqa: E402
 from paper_2502_04217_b200 import _dev, _lib  # noqa: E402
 
-NAMES = ["synth_axis0", "synth_axis1", "gram_mid_axis2", "analyze_axis1", "analyze_axis0", "kkt_epilogue"]
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--size", type=int, default=512)
@@ -46,17 +43,20 @@ def main():
     top, bot = _dev.empty(n), _dev.empty(n)
     buf = (ctypes.c_double * 8)()
     cnt = ctypes.c_int()
-    acc = np.zeros(6)
+    from bench import pass_layout
+
+    names, alg = pass_layout(plan.handle, n, 3)
+    acc = np.zeros(len(names))
     for i in range(args.reps + 3):
         _lib.call("fl_kkt_apply_profiled", plan.handle, _dev.ptr(dm.bits), _dev.ptr(sig1), _dev.ptr(sig2),
                   _dev.ptr(d[:n]), _dev.ptr(d[n:]), _dev.ptr(top), _dev.ptr(bot), buf, ctypes.byref(cnt),
                   _dev.stream())
         if i >= 3:
-            acc += np.array(buf[:6])
+            acc += np.array(buf[:len(names)])
     ms = acc / args.reps
-    alg = [16.0 * n, 16.0 * n, 16.125 * n, 16.0 * n, 16.0 * n, 56.0 * n]
-    out = {"size": side, "passes": {k: {"ms": round(float(m), 4), "GBps": round(a / m / 1e6, 1)}
-                                    for k, m, a in zip(NAMES, ms, alg)},
+    out = {"size": side, "order": "B" if names[-1].endswith("kkt_epilogue") and len(names) == 5 else "A",
+           "passes": {k: {"ms": round(float(m), 4), "GBps": round(a / m / 1e6, 1)}
+                      for k, m, a in zip(names, ms, alg)},
            "total_ms": round(float(ms.sum()), 4), "matvec_per_s": round(1e3 / float(ms.sum()), 2)}
     print(json.dumps(out), flush=True)
 
