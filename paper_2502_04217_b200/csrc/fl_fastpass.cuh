@@ -19,6 +19,7 @@
 #include <mutex>
 #include <unordered_map>
 #include <string>
+#include <type_traits>
 
 #include "fl_common.cuh"
 #include "fl_fast.cuh"
@@ -512,6 +513,22 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
     const bool valid = g < A.G;
     const Geo Q = geo<STRIDED>(A, valid ? g : 0);
     const int64_t next = tile + gridDim.x;
+    // the fused gram addresses its strided rows at 32-bit element offsets from
+    // the pair's base (k * st < 2^32: the launcher refuses larger fibres), so
+    // no 64-bit row address stays live across its two FFTs (fewer spills at
+    // the 128-register cap: 0.79 -> 0.78 ms at 512^3; the one-FFT passes
+    // measured slower with it and keep 64-bit offsets)
+    using Off = std::conditional_t<KIND == K_GRAM, uint32_t, int64_t>;
+    const double* bin = A.in + Q.bx;
+    double* bout = A.out + Q.bx;
+    const Off st32 = (Off)Q.st;
+    auto ld = [&](int k) -> double2 {
+      if constexpr (STRIDED && PIPE == 0) {
+        return valid ? *reinterpret_cast<const double2*>(bin + (Off)k * st32) : make_double2(0.0, 0.0);
+      } else {
+        return raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, k, c);
+      }
+    };
     if constexpr (SMASK) {  // the previous tile's reads ended at its forward FFT's first barrier
       const Geo Q0 = geo<STRIDED>(A, tile * W);
       const uint32_t* wb = A.bits + (Q0.bx >> 5);
@@ -528,7 +545,7 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
       for (int b = 0; b < 2; ++b)
 #pragma unroll
         for (int s = 0; s < 8; ++s)
-          v[8 * b + s] = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, mirror::slot_k<M>(q, b, s), c);
+          v[8 * b + s] = ld(mirror::slot_k<M>(q, b, s));
     } else {
       // Zin_j and Zin_{M-j} from ONE read of the packed rows (j+1, j+H) of
       // j = min(k, M-k); the two values land in the mirror slot pair.
@@ -555,8 +572,8 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
         const int j = i < 4 ? q + i * NB : jb1 + (7 - i) * NB;
         const bool sp = i == 0 && q0;
         double2 a, bb;
-        a = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, sp ? 0 : j + 1, c);
-        bb = raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, sp ? 1 : j + H, c);
+        a = ld(sp ? 0 : j + 1);
+        bb = ld(sp ? 1 : j + H);
         double2 l = lo(a, bb), h = hi(a, bb);
         if constexpr (i == 0) {
           l = sp ? make_double2(c0 * a.x, c0 * a.y) : l;
@@ -569,6 +586,21 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
       });
     }
     refill<M, STRIDED, CFG>(A, next, ntiles, stage0, c, q);
+    if constexpr (STRIDED && PIPE == 0 && M == 1024) {
+      // m = 1024 (one 512-thread CTA per SM): the next tile's M row segments
+      // (W pairs x 16 B each) into L2 while this tile runs its FFT, so DRAM
+      // keeps streaming through the compute phase.  Only at short strides
+      // (axis 1 of 1024^3: 8 KiB, the tile spans one 8 MiB block): 4.75 ->
+      // 4.16 ms (synthesis), 4.83 -> 4.01 ms (analysis); at the 8 MiB stride of
+      // axis 0 it measured neutral, and at m = 512 (two CTAs per SM) slower.
+      if ((next + 1) * W <= A.G && ((A.inner >> 1) % W) == 0) {
+        const Geo Qn = geo<STRIDED>(A, next * W);
+        if (Qn.st <= (int64_t(1) << 16)) {
+          for (int k = threadIdx.x; k < M; k += G::T)
+            fast::bulk_prefetch_l2(A.in + Qn.bx + (int64_t)k * Qn.st, W * 16u);
+        }
+      }
+    }
     // mask bits of the 16 slots (x: bit 2i, y: bit 2i+1) packed into one
     // register before the inverse FFT, so no mask word stays live across it
     uint32_t mbits = 0;
@@ -616,7 +648,7 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
 #pragma unroll
             for (int s = 0; s < 8; ++s) {
               const int64_t t = mirror::slot_k<M>(q, b, s);
-              if (STRIDED) *reinterpret_cast<double2*>(A.out + Q.bx + t * Q.st) = v[8 * b + s];
+              if (STRIDED) *reinterpret_cast<double2*>(bout + (Off)t * st32) = v[8 * b + s];
               else {
                 A.out[Q.bx + t] = v[8 * b + s].x;
                 if (Q.by >= 0) A.out[Q.by + t] = v[8 * b + s].y;
@@ -668,13 +700,13 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
           const int j = mirror::slot_k<M>(q, b, s);
           const double2 a = v[8 * b + s];
           double xa, xb, ya, yb;
-          int64_t ia, ib;
+          Off ia, ib;
           if (b == 0 && s == 0 && q0) {
             const double2 zh = v[4];  // Z_H of q = 0
             xa = c0 * a.x; ya = c0 * a.y;
             xb = c0 * zh.x; yb = c0 * zh.y;
             ia = 0;
-            ib = Q.st;
+            ib = st32;
           } else {
             // mirror partner of slot (b, s) (indices are constants after unrolling)
             const double2 m = q0 ? v[8 * b + (b == 0 ? ((8 - s) & 7) : (7 - s))] : v[8 * (1 - b) + 7 - s];
@@ -682,12 +714,12 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
             xb = c1 * (a.y - m.y);
             ya = c1 * (a.y + m.y);
             yb = c1 * (m.x - a.x);
-            ia = Q.st * (j + 1);
-            ib = Q.st * (j + H);
+            ia = st32 * (Off)(j + 1);
+            ib = st32 * (Off)(j + H);
           }
           if (STRIDED && !EPI) {
-            *reinterpret_cast<double2*>(A.out + Q.bx + ia) = make_double2(xa, ya);
-            *reinterpret_cast<double2*>(A.out + Q.bx + ib) = make_double2(xb, yb);
+            *reinterpret_cast<double2*>(bout + ia) = make_double2(xa, ya);
+            *reinterpret_cast<double2*>(bout + ib) = make_double2(xb, yb);
           } else if (STRIDED) {
             kkt_store2(A, Q.bx + ia, xa, ya, acc);
             kkt_store2(A, Q.bx + ib, xb, yb, acc);

@@ -57,10 +57,22 @@ __device__ __forceinline__ void stage(double2* v, int q, const double2* tw, int 
     if constexpr (NS > 1) {
       const int qq = own(q, b, G::NB);
       const int j = qq % NS;
-      double2 w[8];
-      fast::twiddles<TM, 8, NS>(w, j, tw, sign);
-#pragma unroll
-      for (int s = 1; s < 8; ++s) u[s] = cmul(u[s], w[s]);
+      // fast::twiddles' products applied as they are formed (the same values):
+      // w1, w2, w4 from the table, w3 = w1 w2, w5 = w1 w4, w6 = w2 w4,
+      // w7 = w3 w4, with at most four twiddles live (register pressure of the
+      // two-FFT fused passes)
+      constexpr int step = TM / (NS * 8);
+      const double2 w1 = twiddle(tw, j * step, sign);
+      const double2 w2 = twiddle(tw, 2 * j * step, sign);
+      const double2 w4 = twiddle(tw, 4 * j * step, sign);
+      u[1] = cmul(u[1], w1);
+      u[2] = cmul(u[2], w2);
+      u[4] = cmul(u[4], w4);
+      u[5] = cmul(u[5], cmul(w1, w4));
+      u[6] = cmul(u[6], cmul(w2, w4));
+      const double2 w3 = cmul(w1, w2);
+      u[3] = cmul(u[3], w3);
+      u[7] = cmul(u[7], cmul(w3, w4));
     }
     dft8(u, sign);
   }
