@@ -253,8 +253,10 @@ def run_b200(args, rank: int, world: int):
     traffic = None
     try:  # ncu dram bytes per launch of the same kernel, committed under profiles/
         with open(os.path.join(REPO, "profiles", "r02_traffic.json")) as fh:
-            if side == 512:
-                traffic = json.load(fh)["kernels"].get(names[dom])
+            if side == 512:  # the capture of the operator order this plan runs
+                tj = json.load(fh)
+                key = "kernels_order_b" if names == PASS_NAMES_3D_B else "kernels"
+                traffic = tj.get(key, {}).get(names[dom])
     except Exception:
         traffic = None
     roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(alg[dom] / pass_ms[dom] / 1e6, 1),
