@@ -57,7 +57,7 @@ def fetch() -> None:
     print(f"copied {len(os.listdir(SUITE))} files into {SUITE} (git-ignored)")
 
 
-def install_alias() -> None:
+def install_alias(diag_path: str | None = None) -> None:
     sys.path.insert(0, REPO)
     import paper_2502_04217_b200 as gpu
 
@@ -67,7 +67,7 @@ def install_alias() -> None:
         sys.modules[f"fftlasso.{name}"] = mod
         setattr(gpu, name, mod)
     spec = importlib.util.spec_from_file_location("fftlasso.diagnostics",
-                                                  os.path.join(SUITE, "_ref_diagnostics.py"))
+                                                  diag_path or os.path.join(SUITE, "_ref_diagnostics.py"))
     diag = importlib.util.module_from_spec(spec)
     sys.modules["fftlasso.diagnostics"] = diag
     spec.loader.exec_module(diag)
@@ -79,19 +79,21 @@ def install_alias() -> None:
     assert isinstance(sys.modules["fftlasso"], types.ModuleType)
 
 
-def run(args) -> int:
-    if not os.path.isdir(SUITE):
-        raise SystemExit(f"{SUITE} missing: run `python tools/run_reference_suite.py fetch` in the build container")
-    install_alias()
+def run(args, suite: str = SUITE, diag_path: str | None = None) -> int:
+    if not os.path.isdir(suite):
+        raise SystemExit(f"{suite} missing: run `python tools/run_reference_suite.py fetch` in the build container")
+    install_alias(diag_path)
     import pytest
 
-    sys.path.insert(0, SUITE)  # the suite's `from conftest import ...`
-    return pytest.main([SUITE, "-p", "no:cacheprovider", "-o", "addopts=", "--rootdir", SUITE] + list(args))
+    sys.path.insert(0, suite)  # the suite's `from conftest import ...`
+    return pytest.main([suite, "-p", "no:cacheprovider", "-o", "addopts=", "--rootdir", suite] + list(args))
 
 
 if __name__ == "__main__":
     cmd = sys.argv[1] if len(sys.argv) > 1 else "run"
     if cmd == "fetch":
         fetch()
+    elif cmd == "collect-in-place":  # build container: collect /root/reference's suite without copying it
+        sys.exit(run(["--collect-only", "-q"] + sys.argv[2:], suite=REF_TESTS, diag_path=REF_DIAG))
     else:
         sys.exit(run(sys.argv[2:]))
