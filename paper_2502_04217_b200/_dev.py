@@ -87,6 +87,14 @@ _UPLOAD_MIN = 32 << 20
 # NumPy-in apply_kkt at 512^3 on the 16-core GPU host: 7.3 (8 threads) -> 8.2 (16)
 _POOL_WORKERS = max(4, min(16, os.cpu_count() or 4))
 _UPLOAD_CHUNK = 64 << 20
+# upload_chunks: 32 pinned 32 MiB staging slots in flight (NumPy-in apply_kkt at
+# 512^3 on the 16-core GPU host: 8 x 64 MiB 7.76, 16 x 64 MiB 8.09, 32 x 32 MiB
+# 8.50, 32 x 16 MiB 7.46 matvec/s; tools/gpu/e2e_slots_probe.py).  Page-locking
+# the caller's arrays in place instead (cudaHostRegister) is no faster: ~43
+# GB/s serialised in the driver and ~2.5 GB/s when overlapped with the DMA
+# (tools/gpu/host_register_probe2.py).
+_UPLOAD_SLOTS = 32
+_STAGE_CHUNK = 32 << 20
 _pool = None
 _side_streams: dict = {}
 
@@ -143,7 +151,7 @@ def upload_chunks(groups, stream):
 
     if _pool is None:
         _pool = ThreadPoolExecutor(max_workers=_POOL_WORKERS, thread_name_prefix="fl-upload")
-    step = _UPLOAD_CHUNK // 8
+    step = _STAGE_CHUNK // 8
     pieces = []  # (group index, src, dst, lo, hi), pageable ones split into slots
     for gi, grp in enumerate(groups):
         for src, dst, lo, hi in grp:
@@ -152,7 +160,7 @@ def upload_chunks(groups, stream):
             else:
                 for a in range(lo, hi, step):
                     pieces.append((gi, src, dst, a, min(hi, a + step), True))
-    nslot = 8
+    nslot = _UPLOAD_SLOTS
     slots = [torch.empty(step, dtype=F64, pin_memory=True) for _ in range(nslot)]
     slot_free = [None] * nslot  # event: the DMA out of the slot has finished
 
