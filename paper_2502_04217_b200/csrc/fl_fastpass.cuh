@@ -686,7 +686,8 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
               } else {
                 z.y = 0.0;
               }
-              if (KIND == K_GRAM) nrm += z.x * z.x + z.y * z.y;
+              // (the strided gram serves only the KKT apply, never the PCG norm)
+              if (KIND == K_GRAM && !STRIDED) nrm += z.x * z.x + z.y * z.y;
             }
             v[8 * b + s] = z;
           }

@@ -257,8 +257,9 @@ int run_pass_n(const fl_plan* p, int axis, int kind, const double* in, double* o
     // only the strided fused gram of the axis-0-last order (kkt_order_b)
     int64_t in_ = 1;
     for (int a = axis + 1; a < p->ndim; ++a) in_ *= p->dims[a];
-    if (kind != K_GRAM || p->dims[axis] != 512 || in_ % 32 != 0)
-      return fail(FL_E_VALUE, "a strided fused mask pass needs the gram kind, m = 512 and rows of 32k voxels");
+    if (kind != K_GRAM || p->dims[axis] != 512 || in_ % 32 != 0 || nrm_partials)
+      return fail(FL_E_VALUE, "a strided fused mask pass needs the gram kind, m = 512, rows of 32k voxels "
+                              "and no norm partials");
   }
   PassArgs A;
   A.in = in;
