@@ -8,3 +8,7 @@ if [ -d reference_suite ]; then timeout 900 python tools/run_reference_suite.py 
 python bench.py --steps 2 --warmup 3 --no-solve --no-cpu-baseline > gpurun_out/f_k_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/f_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-solve --no-cpu-baseline > gpurun_out/f_k_ncu.log 2>&1
+# ncu --set full of the five 512^3 matvec launches (order B) for the traffic / stall summary
+python tools/profile_kkt.py --size 512 --reps 2 > gpurun_out/f_plain2.log 2>&1 && \
+ncu --set full --clock-control none -k regex:"pass|epilogue" -s 5 -c 5 -o /tmp/f_full python tools/profile_kkt.py --size 512 --reps 2 > gpurun_out/f_ncu_full.log 2>&1
+ncu -i /tmp/f_full.ncu-rep --page raw --csv > gpurun_out/f_full_raw.csv 2>&1
