@@ -38,9 +38,8 @@
 namespace fl {
 namespace wpk {
 
-#ifndef FL_WP_MINB
-#define FL_WP_MINB 1
-#endif
+// CTAs per SM asked of __launch_bounds__ (one: 255 registers for the 32 elements per thread)
+constexpr int kWpMinBlocks = 1;
 
 // cos / sin(2 pi m / 32), m = 0..31
 __device__ __forceinline__ constexpr double c32(int m) {
@@ -136,7 +135,7 @@ struct WG {
   static constexpr int WARPS = 8, T = WARPS * 32, PPC = WARPS * PPW;
   static constexpr int WARP_BYTES = PPW * BUF * 16;
   static constexpr int SMEM = WARPS * WARP_BYTES;
-  static constexpr int MINB = FL_WP_MINB;
+  static constexpr int MINB = kWpMinBlocks;
 };
 
 // Inverse FFT: natural layout (slot r = element q + P r) -> slot j * P + k2 =
