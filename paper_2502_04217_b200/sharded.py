@@ -206,11 +206,20 @@ class DistComm(Comm):
 
         # an all-reduce cannot complete on any rank before every rank's stream
         # reached it, i.e. before every rank's exchange kernel has finished
+        # (NCCL: stream-ordered).  A host-side group (gloo) over GPU data orders
+        # nothing on the device, so the stream is drained first.
+        if self.device is None and torch.cuda.is_available() and torch.cuda.is_initialized():
+            torch.cuda.current_stream().synchronize()
         t = torch.zeros(1, dtype=torch.float64, device=self.device if self.device is not None else "cpu")
         self.dist.all_reduce(t, group=self.group)
 
     def reduce_device(self, tensors):
         (t,) = tensors
+        if self.device is None and t.is_cuda:  # host-side group: reduce a host copy
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+            return
         self.dist.all_reduce(t, group=self.group)
 
     def peer_buffers(self, n):
