@@ -173,6 +173,12 @@ class LocalComm(Comm):
         return bufs, [table] * self.world
 
 
+def torch_empty_like(t):
+    import torch
+
+    return torch.empty_like(t)
+
+
 class DistComm(Comm):
     """One shard per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
 
@@ -187,6 +193,11 @@ class DistComm(Comm):
 
     def all_to_all(self, send):
         (s,) = send
+        if self.device is None and s.is_cuda:  # host-side group over GPU slabs
+            h = s.cpu()
+            r = torch_empty_like(h)
+            self.dist.all_to_all_single(r, h, group=self.group)
+            return [r.to(s.device)]
         recv = s.new_empty(s.shape)
         self.dist.all_to_all_single(recv, s, group=self.group)
         return [recv]

@@ -36,10 +36,10 @@ def gather(t, world):
     return [o.numpy() for o in out]
 
 
-def run(comm, dims, beta, flags, bfull, sig1, sig2, dz, P, lam):
+def run(comm, dims, beta, flags, bfull, sig1, sig2, dz, P, lam, exchange="peer"):
     """Sharded gram, residual pass, KKT apply and solve on the ranks of ``comm``."""
-    grid = sh.ShardedGrid(dims, comm, exchange="peer")
-    assert grid.exchange == "peer"
+    grid = sh.ShardedGrid(dims, comm, exchange=exchange)
+    assert grid.exchange == exchange
     geo = grid.geo
     prob = sh.ShardedProblem.from_host(grid, flags, np.where(flags, 0.0, bfull))
     xb = [fl._dev.to_dev(geo.x_slab(beta, r)) for r in comm.ranks]
@@ -79,6 +79,9 @@ def main():
     geo, res = run(comm, dims, beta, flags, bfull, sig1, sig2, dz, world, lam)
     full = {k: geo.from_x(gather(res[k][0], world)) for k in ("gram", "resid", "top", "bottom", "beta")}
     comm.release_peer_buffers()
+    # the NCCL-free fallback exchange (pack -> all-to-all -> unpack) across the processes
+    geo2, res2 = run(comm, dims, beta, flags, bfull, sig1, sig2, dz, world, lam, exchange="a2a")
+    full2 = {k: geo2.from_x(gather(res2[k][0], world)) for k in ("gram", "resid", "top", "bottom", "beta")}
     if r == 0:
         _, emu = run(sh.LocalComm(world), dims, beta, flags, bfull, sig1, sig2, dz, world, lam)
         efull = {k: geo.from_x([t.cpu().numpy() for t in emu[k]]) for k in full}
@@ -86,6 +89,7 @@ def main():
         single = np.asarray(fl.gram(beta, mask))
         out = {"world": world,
                "bitwise_vs_emulated": {k: bool(np.array_equal(full[k], efull[k])) for k in full},
+               "a2a_bitwise_vs_peer": {k: bool(np.array_equal(full2[k], full[k])) for k in full},
                "norm_equal": res["norm"] == emu["norm"],
                "solve": res["solve"], "solve_emulated": emu["solve"],
                "gram_vs_single_gpu": float(np.max(np.abs(full["gram"] - single)) / np.abs(single).max())}

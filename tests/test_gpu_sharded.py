@@ -337,6 +337,7 @@ def test_peer_exchange_across_processes():
     res = json.loads(line)
     assert res["world"] == 2
     assert all(res["bitwise_vs_emulated"].values()), res
+    assert all(res["a2a_bitwise_vs_peer"].values()), res
     assert res["norm_equal"]
     assert res["solve"] == res["solve_emulated"] and res["solve"][0] == "converged", res
     assert res["gram_vs_single_gpu"] <= 1e-12
