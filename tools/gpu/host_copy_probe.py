@@ -6,7 +6,6 @@ concurrently, pageable H2D through the driver.  Prints one JSON line.
 import json
 import os
 import subprocess
-import sys
 import time
 from concurrent.futures import ThreadPoolExecutor
 
