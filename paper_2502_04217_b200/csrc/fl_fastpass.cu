@@ -94,10 +94,10 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
             : group ? (m == 512 ? fpk::make_group_512(kind, epi) : fpk::make_group_2048(kind, epi))
                     : lookup(m, strided, kind, epi);
   if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");
-  // the mirrored strided passes address a fibre's rows at 32-bit element
-  // offsets k * stride from its base (a grid past 2^32 doubles per array does
-  // not fit one GPU's IPM workspace anyway)
-  if (strided && (int64_t)(m - 1) * A.inner >= (int64_t(1) << 32))
+  // the strided fused gram addresses a fibre's rows at 32-bit element offsets
+  // k * stride from its base (a grid past 2^32 doubles per array does not fit
+  // one GPU's IPM workspace anyway)
+  if (strided && kind == K_GRAM && (int64_t)(m - 1) * A.inner >= (int64_t(1) << 32))
     return fail(FL_E_SHAPE, "strided fibre spans 2^32 elements or more");
   int grid_cap = 0, dev = 0;
   FL_CUDA(cudaGetDevice(&dev));
