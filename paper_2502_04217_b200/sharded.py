@@ -952,6 +952,9 @@ def solve(b, mask, config: IpmConfig = IpmConfig(), observer=None, comm: Comm | 
     nl = geo.n_local
     dev = _dev.device()
     bits, bhat = {}, {}
+    # tensors on the wire live where the group's backend wants them: the GPU
+    # for NCCL, host memory for a host-side group (gloo)
+    wire = dev if (not dist_mode or getattr(comm, "device", None) is not None) else torch.device("cpu")
     if is_root:
         flags = np.asarray(mask.missing_bool, dtype=bool).reshape(-1)
         bv = b.detach().cpu().numpy() if _dev.is_device(b) else np.asarray(b, dtype=np.float64).reshape(-1)
@@ -962,20 +965,18 @@ def solve(b, mask, config: IpmConfig = IpmConfig(), observer=None, comm: Comm | 
         targets = range(geo.P) if dist_mode else comm.ranks
         for r in targets:
             wb, yb = _y_inputs(geo, flags, b_hat, r)
-            tb = torch.from_numpy(wb).to(dev)
-            ty = torch.from_numpy(yb).to(dev)
             if dist_mode and r != me:
-                comm.dist.send(tb, dst=r, group=comm.group)
-                comm.dist.send(ty, dst=r, group=comm.group)
+                comm.dist.send(torch.from_numpy(wb).to(wire), dst=r, group=comm.group)
+                comm.dist.send(torch.from_numpy(yb).to(wire), dst=r, group=comm.group)
             else:
-                bits[r], bhat[r] = tb, ty
+                bits[r], bhat[r] = torch.from_numpy(wb).to(dev), torch.from_numpy(yb).to(dev)
         del b_hat
     else:
-        tb = torch.empty((nl + 31) // 32, dtype=torch.int32, device=dev)
-        ty = torch.empty(nl, dtype=torch.float64, device=dev)
+        tb = torch.empty((nl + 31) // 32, dtype=torch.int32, device=wire)
+        ty = torch.empty(nl, dtype=torch.float64, device=wire)
         comm.dist.recv(tb, src=root, group=comm.group)
         comm.dist.recv(ty, src=root, group=comm.group)
-        bits[me], bhat[me] = tb, ty
+        bits[me], bhat[me] = tb.to(dev), ty.to(dev)
     prob = ShardedProblem(grid, [bits[r] for r in comm.ranks], [bhat[r] for r in comm.ranks])
     lam = config.lam
     if lam is None:  # default_penalty: 0.1 max|A^T Z b_hat| from one residual pass at beta = 0
@@ -994,8 +995,8 @@ def solve(b, mask, config: IpmConfig = IpmConfig(), observer=None, comm: Comm | 
     betas, report = sharded_solve(prob, lam, config, observer)
     out = None
     if dist_mode:
-        parts = [torch.empty(nl, dtype=torch.float64, device=dev) for _ in range(geo.P)] if me == root else None
-        comm.dist.gather(betas[0].contiguous(), gather_list=parts, dst=root, group=comm.group)
+        parts = [torch.empty(nl, dtype=torch.float64, device=wire) for _ in range(geo.P)] if me == root else None
+        comm.dist.gather(betas[0].contiguous().to(wire), gather_list=parts, dst=root, group=comm.group)
         if me == root:
             out = torch.cat(parts).cpu().numpy()
     else:

@@ -82,7 +82,17 @@ def main():
     # the NCCL-free fallback exchange (pack -> all-to-all -> unpack) across the processes
     geo2, res2 = run(comm, dims, beta, flags, bfull, sig1, sig2, dz, world, lam, exchange="a2a")
     full2 = {k: geo2.from_x(gather(res2[k][0], world)) for k in ("gram", "resid", "top", "bottom", "beta")}
+    # the drop-in API across the processes: root holds the reference arguments
+    mask_full = fl.Mask.from_bool(flags, fl.GridShape(dims))
+    b_obs = bfull[~flags]
+    beta_d, rep_d = sh.solve(b_obs if r == 0 else None, mask_full if r == 0 else None, fl.IpmConfig(lam=lam),
+                             comm=sh.DistComm())
     if r == 0:
+        beta_1, rep_1 = fl.solve(b_obs, mask_full, fl.IpmConfig(lam=lam))
+        dropin = {"status": [rep_d.status, rep_1.status], "iterations": [rep_d.iterations, rep_1.iterations],
+                  "krylov": [list(rep_d.krylov_counts), list(rep_1.krylov_counts)],
+                  "objective_rel": abs(rep_d.final_objective - rep_1.final_objective) / abs(rep_1.final_objective),
+                  "beta_rel_l2": float(np.linalg.norm(beta_d - beta_1) / np.linalg.norm(beta_1))}
         _, emu = run(sh.LocalComm(world), dims, beta, flags, bfull, sig1, sig2, dz, world, lam)
         efull = {k: geo.from_x([t.cpu().numpy() for t in emu[k]]) for k in full}
         mask = fl.Mask.from_bool(flags, fl.GridShape(dims))
@@ -92,7 +102,8 @@ def main():
                "a2a_bitwise_vs_peer": {k: bool(np.array_equal(full2[k], full[k])) for k in full},
                "norm_equal": res["norm"] == emu["norm"],
                "solve": res["solve"], "solve_emulated": emu["solve"],
-               "gram_vs_single_gpu": float(np.max(np.abs(full["gram"] - single)) / np.abs(single).max())}
+               "gram_vs_single_gpu": float(np.max(np.abs(full["gram"] - single)) / np.abs(single).max()),
+               "dropin_vs_single_gpu": dropin}
         print(json.dumps(out), flush=True)
     dist.barrier()
     dist.destroy_process_group()

@@ -341,3 +341,7 @@ def test_peer_exchange_across_processes():
     assert res["norm_equal"]
     assert res["solve"] == res["solve_emulated"] and res["solve"][0] == "converged", res
     assert res["gram_vs_single_gpu"] <= 1e-12
+    d = res["dropin_vs_single_gpu"]  # sharded.solve (reference arguments on root) vs fl.solve on one GPU
+    assert d["status"] == ["converged", "converged"] and d["iterations"][0] == d["iterations"][1]
+    assert all(abs(a - b) <= 1 for a, b in zip(*d["krylov"]))
+    assert d["objective_rel"] <= 1e-9 and d["beta_rel_l2"] <= 1e-8
