@@ -345,3 +345,31 @@ def test_peer_exchange_across_processes():
     assert d["status"] == ["converged", "converged"] and d["iterations"][0] == d["iterations"][1]
     assert all(abs(a - b) <= 1 for a, b in zip(*d["krylov"]))
     assert d["objective_rel"] <= 1e-9 and d["beta_rel_l2"] <= 1e-8
+
+
+def test_bench_multiprocess_path_gloo():
+    """The bench's N > 1 code path (torchrun, one process per rank, one JSON
+    line from rank 0: sharded matvec + sharded C4-recipe solve) with two
+    processes sharing the GPU over a gloo group -- what the driver's scaling
+    run executes over NCCL, checked end to end (timings meaningless here)."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(REPO, "bench.py"),
+           "--dist-backend", "gloo", "--size", "64", "--steps", "2", "--warmup", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=REPO)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-3000:]  # rank 0 alone prints
+    res = json.loads(lines[0])
+    assert res["n_gpus"] == 2 and res["value"] > 0 and res["config"]["parallelism"] == "slab x2"
+    sol = res["solve"]
+    assert sol["status"] == "converged" and sol["support_exact"] and sol["exchange"] == "peer", sol
