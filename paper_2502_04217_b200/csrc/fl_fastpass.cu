@@ -20,7 +20,7 @@ Entry make_4096(bool strided, int kind, bool epi);
 Entry make_8192(bool strided, int kind, bool epi);
 Entry make_mirror_1024(int kind);
 Entry make_group_512(int kind, bool epi);
-Entry make_warp_1024(int kind, bool epi);
+Entry make_warp_1024(int kind, bool epi, bool nrm);
 Entry make_group_2048(int kind, bool epi);
 
 Entry lookup(int m, bool strided, int kind, bool epi) {
@@ -90,7 +90,7 @@ int launch_fast(int m, bool strided, int kind, bool epi, const PassArgs& A, int*
   // FFT's own flop count), not exchange bound.
   const bool warp = !strided && m == 1024;
   Entry e = mir ? fpk::make_mirror_1024(kind)
-            : warp ? fpk::make_warp_1024(kind, epi)
+            : warp ? fpk::make_warp_1024(kind, epi, A.nrm_partials != nullptr)
             : group ? (m == 512 ? fpk::make_group_512(kind, epi) : fpk::make_group_2048(kind, epi))
                     : lookup(m, strided, kind, epi);
   if (!e.fn) return fail(FL_E_VALUE, "no fast kernel for this pass");

@@ -12,7 +12,7 @@ Entry make_4096(bool strided, int kind, bool epi) { return make_any<4096>(stride
 Entry make_8192(bool strided, int kind, bool epi) { return make_any<8192>(strided, kind, epi); }
 
 // contiguous m = 1024: two-stage warp passes (fl_wpass.cuh); 2048: group-decoupled passes (fl_gpass.cuh)
-Entry make_warp_1024(int kind, bool epi) { return wpk::make_warp<1024>(kind, epi); }
+Entry make_warp_1024(int kind, bool epi, bool nrm) { return wpk::make_warp<1024>(kind, epi, nrm); }
 Entry make_group_2048(int kind, bool epi) { return gpk::make_group<2048>(kind, epi); }
 
 // strided m = 1024: the mirrored 8 x 16 x 8 engine (fl_mirror.cuh)
