@@ -67,7 +67,10 @@ def main():
                 except ValueError:
                     pass
         top = ", ".join(f"{n} {v:.1f}" for v, n in sorted(stalls, reverse=True)[:3])
-        lines.append(f"| `{short[:60]}` | {float(g(r, 'gpu__time_duration.sum') or 0):.4f} | {rd_gb:.3f} | {wr_gb:.3f} | {ratio} | "
+        tu = units[col["gpu__time_duration.sum"]] if "gpu__time_duration.sum" in col else "msecond"
+        ms = float(g(r, "gpu__time_duration.sum") or 0) * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+                                                           "second": 1e3}.get(tu, 1.0)
+        lines.append(f"| `{short[:60]}` | {ms:.4f} | {rd_gb:.3f} | {wr_gb:.3f} | {ratio} | "
                      f"{float(g(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed') or 0):.1f} | "
                      f"{float(g(r, 'smsp__issue_active.avg.pct_of_peak_sustained_active') or 0):.1f} | "
                      f"{float(g(r, 'sm__warps_active.avg.pct_of_peak_sustained_active') or 0):.1f} | "
