@@ -68,7 +68,7 @@ def main():
                     pass
         top = ", ".join(f"{n} {v:.1f}" for v, n in sorted(stalls, reverse=True)[:3])
         tu = units[col["gpu__time_duration.sum"]] if "gpu__time_duration.sum" in col else "msecond"
-        ms = float(g(r, "gpu__time_duration.sum") or 0) * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+        ms = float(g(r, "gpu__time_duration.sum") or 0) * {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3,
                                                            "second": 1e3}.get(tu, 1.0)
         lines.append(f"| `{short[:60]}` | {ms:.4f} | {rd_gb:.3f} | {wr_gb:.3f} | {ratio} | "
                      f"{float(g(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed') or 0):.1f} | "
