@@ -527,7 +527,14 @@ __global__ void __launch_bounds__(mirror::MGeom<M, TT>::T, MB) mirror_pass(const
         // strided rows bypass L1 (no reuse; it stays with the spill slots of the
         // 128-register FFTs): fused gram 0.775 -> 0.769 ms, analysis axis 1 at
         // 512^3 0.385 -> 0.371 ms, 1024^3 matvec 32.36 -> 32.20 ms
-        return valid ? __ldcg(reinterpret_cast<const double2*>(bin + (Off)k * st32)) : make_double2(0.0, 0.0);
+        // ld.global.cg with a 256-byte L2 fetch: the neighbouring tile's half
+        // of each 256-byte row segment (the next CTA's) arrives with this one
+        // (512^3 matvec 3.133 -> 3.116 ms; neutral at 1024^3)
+        double2 z = make_double2(0.0, 0.0);
+        if (valid)
+          asm volatile("ld.global.cg.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(z.x), "=d"(z.y)
+                       : "l"(bin + (Off)k * st32));
+        return z;
       } else {
         return raw<M, STRIDED, (PIPE > 0), CFG>(A, stage0, Q, valid, k, c);
       }
